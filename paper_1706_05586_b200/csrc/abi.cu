@@ -1,0 +1,763 @@
+// C-ABI layer of the B200 DOT library: problem state, workspace, field caches
+// and the paper-level calls set_params / misfit / jacobian / optimize_directions
+// (include/dot_b200.h documents every entry point).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "arena.h"
+#include "kernels.h"
+#include "optimize.h"
+
+using namespace dot;
+
+struct FieldCache {
+    bool valid = false;
+    bool identity = false;
+    int ncols = 0;
+    std::vector<double> coeff;        // [n_side][ncols] host copy (empty for identity)
+    DBuf<double2> X;                  // [n_freq][ncols][nP]
+};
+
+struct dot_problem {
+    // ---- configuration
+    int nx = 0, ny = 0, nz = 0, n_freq = 0, n_src = 0, n_det = 0, n_rbf = 0, n_p = 0, max_iter = 0;
+    size_t N = 0;
+    double Lx = 0, Ly = 0, Lz = 0, D = 0, mua_in = 0, mua_out = 0, nu = 0, gamma = 0, eps = 0,
+           cutoff = 0, tol = 0;
+    double hx = 0, hy = 0, hz = 0;
+    std::vector<double> omega;
+    std::vector<int32_t> src, det;
+    std::vector<double> src_scale, det_scale;
+    OpConst op{};
+    CocgTiling tl{};
+    PalsConst pc{};
+    cudaStream_t stream = nullptr;
+    std::string err;
+
+    // ---- device state
+    Arena arena;
+    DBuf<int32_t> d_src, d_det;
+    DBuf<double> d_src_scale, d_det_scale, d_omega_nu, d_mu, d_params;
+    DBuf<int32_t> d_flagS, d_flagP, d_posS, d_posP, d_scan_tmp, d_tot;
+    DBuf<int> d_count;
+    bool have_params = false, have_data = false;
+    std::vector<double> params;
+    // support S and sample set P = S u detectors
+    int K = 0, nP = 0;
+    DBuf<int32_t> d_S, d_P, d_S_slot, d_det_slot, d_off;
+    DBuf<double> d_G;
+    DBuf<double2> d_Dt;               // data, [n_freq][n_src][n_det]
+    FieldCache cache[2];              // 0: sources, 1: detectors
+
+    // ---- stats / timing
+    dot_stats stats{};
+    bool timing = false;
+    std::vector<cudaEvent_t> events;
+    int* h_count = nullptr;
+
+    ~dot_problem() {
+        for (auto e : events) cudaEventDestroy(e);
+        if (h_count) cudaFreeHost(h_count);
+    }
+};
+
+namespace {
+
+std::string g_create_error;
+
+void sync(dot_problem* P) { DOT_CUDA_TRY(cudaStreamSynchronize(P->stream)); }
+
+cudaEvent_t event_at(dot_problem* P, size_t i) {
+    while (P->events.size() <= i) {
+        cudaEvent_t e;
+        DOT_CUDA_TRY(cudaEventCreate(&e));
+        P->events.push_back(e);
+    }
+    return P->events[i];
+}
+
+void require_bound(dot_problem* P) {
+    if (!P->arena.bound()) throw Error(DOT_ERR_STATE, "no workspace bound (dot_bind_workspace)");
+}
+void require_params(dot_problem* P) {
+    require_bound(P);
+    if (!P->have_params) throw Error(DOT_ERR_STATE, "no parameters (dot_set_params)");
+}
+
+// copy `count` elements of T from (host|device) src to a device buffer
+template <class T>
+DBuf<T> to_device(dot_problem* P, const T* src, size_t count, int where) {
+    DBuf<T> b(P->arena, std::max<size_t>(count, 1));
+    if (count) {
+        DOT_CUDA_TRY(cudaMemcpyAsync(b.get(), src, count * sizeof(T),
+                                     where == DOT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                                     P->stream));
+    }
+    return b;
+}
+
+template <class T>
+void from_device(dot_problem* P, T* dst, const T* src, size_t count, int where) {
+    if (!count) return;
+    DOT_CUDA_TRY(cudaMemcpyAsync(dst, src, count * sizeof(T),
+                                 where == DOT_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                                 P->stream));
+    if (where == DOT_HOST) sync(P);
+}
+
+// host copy of a (host|device) real matrix
+std::vector<double> host_copy(dot_problem* P, const double* src, size_t count, int where) {
+    std::vector<double> h(count);
+    if (!count) return h;
+    if (where == DOT_HOST) {
+        std::memcpy(h.data(), src, count * sizeof(double));
+    } else {
+        DOT_CUDA_TRY(cudaMemcpyAsync(h.data(), src, count * sizeof(double), cudaMemcpyDeviceToHost, P->stream));
+        sync(P);
+    }
+    return h;
+}
+
+size_t per_rhs_bytes(const dot_problem* P) {
+    const size_t vec = P->N * sizeof(double2);
+    return 4 * vec + 2 * P->tl.ntiles * kNumPartials * sizeof(double) + 2 * sizeof(RhsState) +
+           sizeof(double) + 4 * Arena::kAlign;
+}
+
+// ---------------------------------------------------------------- batched solve
+// Solve the global RHS list r = f*ncols + c, f < n_freq, c < ncols, where RHS
+// (f, c) is either the point-combination `side` (0: B coeff[:,c], 1: C coeff[:,c])
+// or, if dense != null, the dense vector dense[r].  Outputs: XP [n_rhs][nP]
+// (sampled) or, if Xfull != null, Xfull [n_rhs][N].  freq_of: optional per-RHS
+// frequency (dense mode).  Returns per-RHS iterations.
+std::vector<int32_t> solve_rhs(dot_problem* P, int side, const double* d_coeff, int ncols, int n_rhs,
+                               const double2* dense, const int32_t* d_freq_of, double2* XP,
+                               double2* Xfull) {
+    std::vector<int32_t> iters(n_rhs, 0);
+    if (n_rhs == 0) return iters;
+    const size_t N = P->N;
+    const size_t prb = per_rhs_bytes(P) + (Xfull ? 0 : 0);
+    size_t fit = P->arena.largest_free() / prb;
+    // multiple allocations fragment the arena: keep a safety margin
+    fit = fit > 2 ? fit - 1 : fit;
+    if (fit < 1) throw Error(DOT_ERR_WORKSPACE, "workspace too small for one right-hand side");
+    const int chunk = (int)std::min<size_t>(fit, (size_t)n_rhs);
+    const int CHK = 8;
+
+    for (int r0 = 0; r0 < n_rhs; r0 += chunk) {
+        const int nb = std::min(chunk, n_rhs - r0);
+        DBuf<double2> R0(P->arena, nb * N), R1(P->arena, nb * N), P0(P->arena, nb * N), P1(P->arena, nb * N);
+        DBuf<double> part(P->arena, 2 * (size_t)nb * P->tl.ntiles * kNumPartials);
+        DBuf<RhsState> st(P->arena, 2 * (size_t)nb);
+        DBuf<double> shift(P->arena, nb);
+
+        // ---- right-hand sides
+        if (dense) {
+            DOT_CUDA_TRY(cudaMemcpyAsync(R0.get(), dense + (size_t)r0 * N, (size_t)nb * N * sizeof(double2),
+                                         cudaMemcpyDeviceToDevice, P->stream));
+        } else {
+            DOT_CUDA_TRY(cudaMemsetAsync(R0.get(), 0, (size_t)nb * N * sizeof(double2), P->stream));
+            const int nn = side == 0 ? P->n_src : P->n_det;
+            launch_scatter_rhs(R0.get(), N, nb, r0, ncols, side == 0 ? P->d_src.get() : P->d_det.get(), nn,
+                               d_coeff, side == 0 ? P->d_src_scale.get() : P->d_det_scale.get(), P->stream);
+            P->stats.kernel_launches++;
+        }
+        if (d_freq_of) {
+            // shift[r] = omega_nu[freq_of[r0 + r]] : reuse fill_shift with ncols = 1 on a gathered table
+            std::vector<int32_t> fh(nb);
+            DOT_CUDA_TRY(cudaMemcpyAsync(fh.data(), d_freq_of + r0, nb * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                         P->stream));
+            sync(P);
+            std::vector<double> sh(nb);
+            for (int r = 0; r < nb; ++r) {
+                if (fh[r] < 0 || fh[r] >= P->n_freq) throw Error(DOT_ERR_ARG, "frequency index out of range");
+                sh[r] = P->omega[fh[r]] / P->nu;
+            }
+            DOT_CUDA_TRY(cudaMemcpyAsync(shift.get(), sh.data(), nb * sizeof(double), cudaMemcpyHostToDevice,
+                                         P->stream));
+            sync(P);
+        } else {
+            launch_fill_shift(shift.get(), nb, r0, ncols, P->d_omega_nu.get(), P->stream);
+            P->stats.kernel_launches++;
+        }
+        if (XP) DOT_CUDA_TRY(cudaMemsetAsync(XP + (size_t)r0 * P->nP, 0, (size_t)nb * P->nP * sizeof(double2), P->stream));
+        if (Xfull) DOT_CUDA_TRY(cudaMemsetAsync(Xfull + (size_t)r0 * N, 0, (size_t)nb * N * sizeof(double2), P->stream));
+
+        PassArgs a;
+        a.op = P->op;
+        a.tl = P->tl;
+        a.max_iter = P->max_iter;
+        a.tol2 = P->tol * P->tol;
+        a.mu = P->d_mu.get();
+        a.shift = shift.get();
+        a.R[0] = R0.get();
+        a.R[1] = R1.get();
+        a.Pv[0] = P0.get();
+        a.Pv[1] = P1.get();
+        a.part[0] = part.get();
+        a.part[1] = part.get() + (size_t)nb * P->tl.ntiles * kNumPartials;
+        a.st[0] = st.get();
+        a.st[1] = st.get() + nb;
+        a.samp_nodes = P->d_P.get();
+        a.samp_off = P->d_off.get();
+        a.XP = XP ? XP + (size_t)r0 * P->nP : nullptr;
+        a.nP = XP ? P->nP : 0;
+        a.X = Xfull ? Xfull + (size_t)r0 * N : nullptr;
+
+        launch_cocg_init(a, nb, P->stream);
+        P->stats.kernel_launches++;
+        int k = 0;
+        size_t ev = 0;
+        for (;;) {
+            if (P->timing && k % CHK == 0) DOT_CUDA_TRY(cudaEventRecord(event_at(P, ev++), P->stream));
+            a.k = k;
+            launch_cocg_pass(a, nb, P->stream);
+            P->stats.kernel_launches++;
+            P->stats.pass_launches++;
+            ++k;
+            if (k % CHK == 0 || k > P->max_iter) {
+                if (P->timing) DOT_CUDA_TRY(cudaEventRecord(event_at(P, ev++), P->stream));
+                launch_count_active(a.st[(k - 1) & 1], nb, P->d_count.get(), P->stream);
+                P->stats.kernel_launches++;
+                DOT_CUDA_TRY(cudaMemcpyAsync(P->h_count, P->d_count.get(), sizeof(int), cudaMemcpyDeviceToHost,
+                                             P->stream));
+                sync(P);
+                if (*P->h_count == 0) break;
+            }
+        }
+        if (P->timing) {
+            for (size_t e = 0; e + 1 < ev; e += 2) {
+                float ms = 0;
+                DOT_CUDA_TRY(cudaEventElapsedTime(&ms, P->events[e], P->events[e + 1]));
+                P->stats.pass_ms += ms;
+            }
+        }
+        std::vector<RhsState> hs(nb);
+        DOT_CUDA_TRY(cudaMemcpyAsync(hs.data(), a.st[(k - 1) & 1], nb * sizeof(RhsState), cudaMemcpyDeviceToHost,
+                                     P->stream));
+        sync(P);
+        int mx = 0, mn = 1 << 30;
+        for (int r = 0; r < nb; ++r) {
+            if (hs[r].flag == DOT_ERR_NOCONV)
+                throw Error(DOT_ERR_NOCONV, "COCG did not converge within max_iter for rhs " + std::to_string(r0 + r));
+            if (hs[r].flag == DOT_ERR_BREAKDOWN)
+                throw Error(DOT_ERR_BREAKDOWN, "COCG breakdown for rhs " + std::to_string(r0 + r));
+            iters[r0 + r] = hs[r].iters;
+            mx = std::max(mx, hs[r].iters);
+            mn = std::min(mn, hs[r].iters);
+            P->stats.rhs_iterations += hs[r].iters;
+            P->stats.pass_bytes += 64.0 * (double)N * hs[r].iters;
+        }
+        P->stats.rhs_solved += nb;
+        P->stats.last_max_iters = mx;
+        P->stats.last_min_iters = mn;
+    }
+    return iters;
+}
+
+// Sampled fields for `side` and coefficients (host copy hc; empty = identity):
+// returns a pointer to [n_freq][ncols][nP]; `tmp` receives storage when the
+// fields are formed by combination rather than taken from the cache.
+const double2* get_fields(dot_problem* P, int side, const std::vector<double>& hc, bool identity, int ncols,
+                          DBuf<double2>& tmp) {
+    const int n_side = side == 0 ? P->n_src : P->n_det;
+    FieldCache& c = P->cache[side];
+    if (c.valid) {
+        if (identity && c.identity) return c.X.get();
+        if (!identity && !c.identity && c.ncols == ncols && c.coeff == hc) return c.X.get();
+        if (!identity && c.identity) {
+            // linear combination of cached full-data fields: X'[f][c][q] = sum_a coeff[a][c] X[f][a][q]
+            DBuf<double> dc = to_device(P, hc.data(), hc.size(), DOT_HOST);
+            tmp = DBuf<double2>(P->arena, (size_t)P->n_freq * ncols * std::max(P->nP, 1));
+            launch_rc_gemm(P->n_freq, ncols, P->nP, n_side, dc.get(), ncols, c.X.get(), (size_t)n_side * P->nP,
+                           P->nP, 1, tmp.get(), (size_t)ncols * P->nP, P->nP, 1, P->stream);
+            P->stats.kernel_launches++;
+            return tmp.get();
+        }
+    }
+    // solve and cache
+    c.valid = false;
+    c.X.reset();
+    c.X = DBuf<double2>(P->arena, (size_t)P->n_freq * ncols * std::max(P->nP, 1));
+    DBuf<double> dc;
+    if (!identity) dc = to_device(P, hc.data(), hc.size(), DOT_HOST);
+    solve_rhs(P, side, identity ? nullptr : dc.get(), ncols, P->n_freq * ncols, nullptr, nullptr, c.X.get(),
+              nullptr);
+    c.valid = true;
+    c.identity = identity;
+    c.ncols = ncols;
+    c.coeff = identity ? std::vector<double>() : hc;
+    return c.X.get();
+}
+
+void invalidate_caches(dot_problem* P) {
+    for (auto& c : P->cache) {
+        c.valid = false;
+        c.X.reset();
+        c.coeff.clear();
+    }
+}
+
+int fail(dot_problem* P, const Error& e) {
+    if (P) P->err = e.msg;
+    else g_create_error = e.msg;
+    return e.code;
+}
+
+#define DOT_API_BEGIN try {
+#define DOT_API_END(P)                                 \
+    }                                                  \
+    catch (const Error& e) { return fail(P, e); }      \
+    catch (const std::exception& e) { return fail(P, Error(DOT_ERR_ARG, e.what())); } \
+    return DOT_OK;
+
+void check_side_matrix(const double* M, int n_side, int ncols, const char* name) {
+    if (ncols <= 0) throw Error(DOT_ERR_ARG, std::string(name) + ": number of columns must be positive");
+    if (!M && ncols != n_side) throw Error(DOT_ERR_ARG, std::string(name) + " = NULL (identity) needs ncols = n");
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+const char* dot_version(void) { return "dot_b200 0.1 (sm_100a)"; }
+
+const char* dot_last_error(const dot_problem* P) { return P ? P->err.c_str() : g_create_error.c_str(); }
+
+int dot_create(const dot_config* cfg, dot_problem** out) {
+    dot_problem* P = nullptr;
+    try {
+        if (!cfg || !out) throw Error(DOT_ERR_ARG, "null argument");
+        if (cfg->nx < 1 || cfg->ny < 1 || cfg->nz < 2) throw Error(DOT_ERR_ARG, "need nx, ny >= 1, nz >= 2");
+        if (cfg->nx > 256) throw Error(DOT_ERR_ARG, "nx > 256 not supported");
+        if (!(cfg->Lx > 0 && cfg->Ly > 0 && cfg->Lz > 0 && cfg->D > 0 && cfg->nu > 0))
+            throw Error(DOT_ERR_ARG, "extents, D and nu must be positive");
+        if (cfg->n_freq < 1 || !cfg->omega) throw Error(DOT_ERR_ARG, "need at least one frequency");
+        if (cfg->n_src < 1 || cfg->n_det < 1 || !cfg->src_nodes || !cfg->det_nodes)
+            throw Error(DOT_ERR_ARG, "need sources and detectors");
+        if (cfg->n_rbf < 0) throw Error(DOT_ERR_ARG, "n_rbf < 0");
+        if (!(cfg->gamma > 0 && cfg->eps > 0)) throw Error(DOT_ERR_ARG, "gamma and eps must be positive");
+        std::unique_ptr<dot_problem> p(new dot_problem());
+        P = p.get();
+        P->nx = cfg->nx; P->ny = cfg->ny; P->nz = cfg->nz;
+        P->N = (size_t)cfg->nx * cfg->ny * cfg->nz;
+        if (P->N >= (1ull << 31)) throw Error(DOT_ERR_ARG, "grid too large (N >= 2^31)");
+        P->Lx = cfg->Lx; P->Ly = cfg->Ly; P->Lz = cfg->Lz;
+        P->D = cfg->D; P->mua_in = cfg->mua_in; P->mua_out = cfg->mua_out; P->nu = cfg->nu;
+        P->gamma = cfg->gamma; P->eps = cfg->eps; P->cutoff = cfg->cutoff;
+        P->tol = cfg->tol > 0 ? cfg->tol : 1e-17;
+        P->max_iter = cfg->max_iter > 0 ? cfg->max_iter : 4000;
+        P->n_freq = cfg->n_freq; P->n_src = cfg->n_src; P->n_det = cfg->n_det;
+        P->n_rbf = cfg->n_rbf; P->n_p = 5 * cfg->n_rbf;
+        P->omega.assign(cfg->omega, cfg->omega + cfg->n_freq);
+        P->hx = P->Lx / (P->nx + 1);
+        P->hy = P->Ly / (P->ny + 1);
+        P->hz = P->Lz / (P->nz - 1);
+        const double V = P->hx * P->hy * P->hz;
+        auto take_nodes = [&](const int64_t* nodes, int n, std::vector<int32_t>& dst, std::vector<double>& scale,
+                              bool source) {
+            std::vector<int64_t> sorted(nodes, nodes + n);
+            std::sort(sorted.begin(), sorted.end());
+            if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+                throw Error(DOT_ERR_ARG, "duplicate node on one side");
+            for (int a = 0; a < n; ++a) {
+                if (nodes[a] < 0 || (size_t)nodes[a] >= P->N) throw Error(DOT_ERR_ARG, "node index out of range");
+                dst.push_back((int32_t)nodes[a]);
+                const int k = (int)(nodes[a] / ((int64_t)P->nx * P->ny));
+                const double th = (k == 0 || k == P->nz - 1) ? 0.5 : 1.0;
+                scale.push_back(source ? th / V : 1.0);      // b_s = theta e/(hx hy hz), c_d = e (R6)
+            }
+        };
+        take_nodes(cfg->src_nodes, cfg->n_src, P->src, P->src_scale, true);
+        take_nodes(cfg->det_nodes, cfg->n_det, P->det, P->det_scale, false);
+        P->op.nx = P->nx; P->op.ny = P->ny; P->op.nz = P->nz;
+        P->op.cx = P->D / (P->hx * P->hx);
+        P->op.cy = P->D / (P->hy * P->hy);
+        P->op.cz = P->D / (P->hz * P->hz);
+        P->op.robin = 1.0 / (2.0 * P->hz);
+        P->tl = cocg_tiling(P->nx, P->ny, P->nz);
+        P->pc = PalsConst{P->nx, P->ny, P->nz, P->n_rbf, P->hx, P->hy, P->hz, P->gamma, P->eps, P->cutoff,
+                          P->mua_in, P->mua_out};
+        DOT_CUDA_TRY(cudaMallocHost(&P->h_count, sizeof(int)));
+        *out = p.release();
+        return DOT_OK;
+    } catch (const Error& e) {
+        g_create_error = e.msg;
+        return e.code;
+    }
+}
+
+int dot_destroy(dot_problem* P) {
+    if (!P) return DOT_OK;
+    try {
+        if (P->stream || true) cudaStreamSynchronize(P->stream);
+    } catch (...) {
+    }
+    delete P;
+    return DOT_OK;
+}
+
+int dot_set_stream(dot_problem* P, void* s) {
+    DOT_API_BEGIN
+    if (!P) throw Error(DOT_ERR_ARG, "null problem");
+    P->stream = static_cast<cudaStream_t>(s);
+    DOT_API_END(P)
+}
+
+size_t dot_workspace_bytes(const dot_problem* P, int32_t max_rhs) {
+    if (!P) return 0;
+    const size_t N = P->N;
+    size_t fixed = N * (sizeof(double) + 4 * sizeof(int32_t)) + scan_temp_bytes(N) + 64 * 1024;
+    // support / samples: budget 5% of the nodes
+    const size_t Kb = N / 20 + P->n_det;
+    fixed += Kb * (3 * sizeof(int32_t) + P->n_p * sizeof(double)) + (size_t)P->nz * P->tl.ntiles * 4;
+    fixed += (size_t)P->n_freq * P->n_src * P->n_det * sizeof(double2);
+    // field caches (sources + detectors, all frequencies) on the samples
+    fixed += (size_t)P->n_freq * (P->n_src + P->n_det) * Kb * sizeof(double2);
+    return fixed + (size_t)std::max(max_rhs, 1) * per_rhs_bytes(P) + 64 * Arena::kAlign;
+}
+
+int dot_bind_workspace(dot_problem* P, void* ptr, size_t bytes) {
+    DOT_API_BEGIN
+    if (!P || !ptr) throw Error(DOT_ERR_ARG, "null argument");
+    if ((reinterpret_cast<uintptr_t>(ptr) & 255) != 0) throw Error(DOT_ERR_ARG, "workspace must be 256-byte aligned");
+    // drop everything allocated from the old workspace
+    invalidate_caches(P);
+    P->d_S.reset(); P->d_P.reset(); P->d_S_slot.reset(); P->d_det_slot.reset(); P->d_off.reset(); P->d_G.reset();
+    P->d_Dt.reset(); P->d_src.reset(); P->d_det.reset(); P->d_src_scale.reset(); P->d_det_scale.reset();
+    P->d_omega_nu.reset(); P->d_mu.reset(); P->d_params.reset(); P->d_flagS.reset(); P->d_flagP.reset();
+    P->d_posS.reset(); P->d_posP.reset(); P->d_scan_tmp.reset(); P->d_tot.reset(); P->d_count.reset();
+    P->have_params = P->have_data = false;
+    P->arena.reset(ptr, bytes);
+    const size_t N = P->N;
+    P->d_src = to_device(P, P->src.data(), P->src.size(), DOT_HOST);
+    P->d_det = to_device(P, P->det.data(), P->det.size(), DOT_HOST);
+    P->d_src_scale = to_device(P, P->src_scale.data(), P->src_scale.size(), DOT_HOST);
+    P->d_det_scale = to_device(P, P->det_scale.data(), P->det_scale.size(), DOT_HOST);
+    std::vector<double> wn(P->n_freq);
+    for (int f = 0; f < P->n_freq; ++f) wn[f] = P->omega[f] / P->nu;
+    P->d_omega_nu = to_device(P, wn.data(), wn.size(), DOT_HOST);
+    P->d_mu = DBuf<double>(P->arena, N);
+    P->d_params = DBuf<double>(P->arena, std::max(P->n_p, 1));
+    P->d_flagS = DBuf<int32_t>(P->arena, N);
+    P->d_flagP = DBuf<int32_t>(P->arena, N);
+    P->d_posS = DBuf<int32_t>(P->arena, N);
+    P->d_posP = DBuf<int32_t>(P->arena, N);
+    P->d_scan_tmp = DBuf<int32_t>(P->arena, scan_temp_bytes(N) / 4 + 1);
+    P->d_tot = DBuf<int32_t>(P->arena, 4);
+    P->d_count = DBuf<int>(P->arena, 4);
+    sync(P);
+    DOT_API_END(P)
+}
+
+int dot_enable_timing(dot_problem* P, int on) {
+    DOT_API_BEGIN
+    if (!P) throw Error(DOT_ERR_ARG, "null problem");
+    P->timing = on != 0;
+    DOT_API_END(P)
+}
+
+int dot_get_stats(const dot_problem* P, dot_stats* out) {
+    if (!P || !out) return DOT_ERR_ARG;
+    *out = P->stats;
+    out->support_K = P->K;
+    out->n_samples = P->nP;
+    return DOT_OK;
+}
+
+int dot_reset_stats(dot_problem* P) {
+    if (!P) return DOT_ERR_ARG;
+    P->stats = dot_stats{};
+    return DOT_OK;
+}
+
+int dot_set_data(dot_problem* P, const double* data, int where) {
+    DOT_API_BEGIN
+    if (!P || !data) throw Error(DOT_ERR_ARG, "null argument");
+    require_bound(P);
+    const size_t n = (size_t)P->n_freq * P->n_det * P->n_src;
+    DBuf<double2> tmp = to_device(P, reinterpret_cast<const double2*>(data), n, where);
+    P->d_Dt.reset();
+    P->d_Dt = DBuf<double2>(P->arena, n);
+    launch_transpose_data(tmp.get(), P->n_freq, P->n_det, P->n_src, P->d_Dt.get(), P->stream);
+    P->stats.kernel_launches++;
+    sync(P);
+    P->have_data = true;
+    DOT_API_END(P)
+}
+
+int dot_set_params(dot_problem* P, const double* p, int where) {
+    DOT_API_BEGIN
+    if (!P || (!p && P->n_p > 0)) throw Error(DOT_ERR_ARG, "null argument");
+    require_bound(P);
+    const size_t N = P->N;
+    invalidate_caches(P);
+    P->params = host_copy(P, p, P->n_p, where);
+    for (double v : P->params)
+        if (!std::isfinite(v)) throw Error(DOT_ERR_ARG, "non-finite parameter");
+    DOT_CUDA_TRY(cudaMemcpyAsync(P->d_params.get(), P->params.data(), P->n_p * sizeof(double), cudaMemcpyHostToDevice,
+                                 P->stream));
+    cudaStream_t s = P->stream;
+    launch_pals_eval(P->pc, P->d_params.get(), P->d_mu.get(), P->d_flagS.get(), P->d_flagP.get(), s);
+    launch_mark_nodes(P->d_flagP.get(), P->d_det.get(), P->n_det, s);
+    launch_mark_nodes(P->d_flagP.get(), P->d_src.get(), P->n_src, s);   // reciprocity / adjoint samples
+    launch_exclusive_scan(P->d_flagS.get(), P->d_posS.get(), N, P->d_tot.get(), P->d_scan_tmp.get(), s);
+    launch_exclusive_scan(P->d_flagP.get(), P->d_posP.get(), N, P->d_tot.get() + 1, P->d_scan_tmp.get(), s);
+    P->stats.kernel_launches += 8;
+    int32_t tot[2];
+    DOT_CUDA_TRY(cudaMemcpyAsync(tot, P->d_tot.get(), 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    sync(P);
+    P->K = tot[0];
+    P->nP = tot[1];
+    P->d_S.reset(); P->d_P.reset(); P->d_S_slot.reset(); P->d_det_slot.reset(); P->d_off.reset(); P->d_G.reset();
+    P->d_S = DBuf<int32_t>(P->arena, std::max(P->K, 1));
+    P->d_P = DBuf<int32_t>(P->arena, std::max(P->nP, 1));
+    P->d_S_slot = DBuf<int32_t>(P->arena, std::max(P->K, 1));
+    P->d_det_slot = DBuf<int32_t>(P->arena, P->n_det);
+    P->d_off = DBuf<int32_t>(P->arena, (size_t)P->nz * P->tl.ntiles + 1);
+    P->d_G = DBuf<double>(P->arena, std::max<size_t>((size_t)P->K * P->n_p, 1));
+    launch_compact(P->d_flagS.get(), P->d_posS.get(), N, P->d_S.get(), s);
+    launch_compact(P->d_flagP.get(), P->d_posP.get(), N, P->d_P.get(), s);
+    launch_gather_rank(P->d_posP.get(), P->d_S.get(), P->K, P->d_S_slot.get(), s);
+    launch_gather_rank(P->d_posP.get(), P->d_det.get(), P->n_det, P->d_det_slot.get(), s);
+    launch_pals_grad(P->pc, P->d_params.get(), P->d_S.get(), P->K, P->d_G.get(), s);
+    launch_sample_offsets(P->d_P.get(), P->nP, P->nx, P->ny, P->nz, P->tl.TY, P->tl.ntiles, P->d_off.get(), s);
+    P->stats.kernel_launches += 6;
+    sync(P);
+    P->have_params = true;
+    DOT_API_END(P)
+}
+
+int dot_misfit(dot_problem* P, const double* W, int32_t ls, const double* V, int32_t ld, int where,
+               double* misfit_out, double* resid_out) {
+    DOT_API_BEGIN
+    if (!P) throw Error(DOT_ERR_ARG, "null problem");
+    require_params(P);
+    if (!P->have_data) throw Error(DOT_ERR_STATE, "no data (dot_set_data)");
+    check_side_matrix(W, P->n_src, ls, "W");
+    check_side_matrix(V, P->n_det, ld, "V");
+    cudaStream_t s = P->stream;
+    const int nf = P->n_freq, ns = P->n_src, nd = P->n_det;
+    std::vector<double> hW = W ? host_copy(P, W, (size_t)ns * ls, where) : std::vector<double>();
+    DBuf<double2> tmpX;
+    const double2* X = get_fields(P, 0, hW, W == nullptr, ls, tmpX);
+    // Mt[f][i][d] = X[f][i][det_slot[d]]
+    DBuf<double2> Rt(P->arena, (size_t)nf * ls * nd);
+    launch_gather_cols(nf, ls, nd, X, (size_t)ls * P->nP, P->nP, P->d_det_slot.get(), Rt.get(), (size_t)ls * nd, nd, s);
+    // DWt[f][i][d] = sum_s W[s][i] Dt[f][s][d]
+    DBuf<double2> DWt(P->arena, (size_t)nf * ls * nd);
+    DBuf<double> dW;
+    if (W) dW = to_device(P, hW.data(), hW.size(), DOT_HOST);
+    launch_rc_gemm(nf, ls, nd, ns, W ? dW.get() : nullptr, ls, P->d_Dt.get(), (size_t)ns * nd, nd, 1, DWt.get(),
+                   (size_t)ls * nd, nd, 1, s);
+    launch_csub_inplace(Rt.get(), DWt.get(), (size_t)nf * ls * nd, s);
+    // S[f][j][i] = sum_d V[d][j] Rt[f][i][d]
+    DBuf<double2> S(P->arena, (size_t)nf * ld * ls);
+    DBuf<double> dV;
+    std::vector<double> hV;
+    if (V) {
+        hV = host_copy(P, V, (size_t)nd * ld, where);
+        dV = to_device(P, hV.data(), hV.size(), DOT_HOST);
+    }
+    launch_rc_gemm(nf, ld, ls, nd, V ? dV.get() : nullptr, ld, Rt.get(), (size_t)ls * nd, 1, nd, S.get(),
+                   (size_t)ld * ls, ls, 1, s);
+    DBuf<double> d_m(P->arena, 1);
+    launch_sumsq(S.get(), (size_t)nf * ld * ls, d_m.get(), s);
+    P->stats.kernel_launches += 5;
+    double m = 0;
+    DOT_CUDA_TRY(cudaMemcpyAsync(&m, d_m.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (resid_out)
+        DOT_CUDA_TRY(cudaMemcpyAsync(resid_out, S.get(), (size_t)nf * ld * ls * sizeof(double2),
+                                     where == DOT_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+    sync(P);
+    if (misfit_out) *misfit_out = m;
+    DOT_API_END(P)
+}
+
+int dot_jacobian(dot_problem* P, const double* W, int32_t ls, const double* V, int32_t ld, int where,
+                 double* J_out) {
+    DOT_API_BEGIN
+    if (!P || !J_out) throw Error(DOT_ERR_ARG, "null argument");
+    require_params(P);
+    check_side_matrix(W, P->n_src, ls, "W");
+    check_side_matrix(V, P->n_det, ld, "V");
+    cudaStream_t s = P->stream;
+    const int nf = P->n_freq, K = P->K;
+    std::vector<double> hW = W ? host_copy(P, W, (size_t)P->n_src * ls, where) : std::vector<double>();
+    std::vector<double> hV = V ? host_copy(P, V, (size_t)P->n_det * ld, where) : std::vector<double>();
+    DBuf<double2> tmpU, tmpL;
+    const double2* XU = get_fields(P, 0, hW, W == nullptr, ls, tmpU);
+    const double2* XL = get_fields(P, 1, hV, V == nullptr, ld, tmpL);
+    const size_t nJ = (size_t)nf * ld * ls * P->n_p;
+    DBuf<double2> Jtmp;
+    double2* J = reinterpret_cast<double2*>(J_out);
+    if (where == DOT_HOST) {
+        Jtmp = DBuf<double2>(P->arena, std::max<size_t>(nJ, 1));
+        J = Jtmp.get();
+    }
+    DBuf<double2> US(P->arena, std::max<size_t>((size_t)nf * ls * K, 1)), LS(P->arena, std::max<size_t>((size_t)nf * ld * K, 1));
+    launch_gather_cols(nf, ls, K, XU, (size_t)ls * P->nP, P->nP, P->d_S_slot.get(), US.get(), (size_t)ls * K, K, s);
+    launch_gather_cols(nf, ld, K, XL, (size_t)ld * P->nP, P->nP, P->d_S_slot.get(), LS.get(), (size_t)ld * K, K, s);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (P->timing) {
+        e0 = event_at(P, 0);
+        e1 = event_at(P, 1);
+        DOT_CUDA_TRY(cudaEventRecord(e0, s));
+    }
+    launch_contract(nf, K, ld, ls, P->n_p, LS.get(), (size_t)ld * K, US.get(), (size_t)ls * K, P->d_G.get(), J, s);
+    P->stats.kernel_launches += 3;
+    if (P->timing) {
+        DOT_CUDA_TRY(cudaEventRecord(e1, s));
+        DOT_CUDA_TRY(cudaEventSynchronize(e1));
+        float ms = 0;
+        DOT_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+        P->stats.contract_ms += ms;
+    }
+    P->stats.contract_flops += 4.0 * nf * ld * ls * (double)K * P->n_p;
+    if (where == DOT_HOST) {
+        DOT_CUDA_TRY(cudaMemcpyAsync(J_out, J, nJ * sizeof(double2), cudaMemcpyDeviceToHost, s));
+    }
+    sync(P);
+    DOT_API_END(P)
+}
+
+int dot_optimize_directions(dot_problem* P, int32_t k, const double* W, int32_t ls, const double* V, int32_t ld,
+                            int where, double* W_out, double* V_out, double* objective_out) {
+    DOT_API_BEGIN
+    if (!P || !W || !V || !W_out || !V_out) throw Error(DOT_ERR_ARG, "null argument");
+    require_params(P);
+    if (k < 0 || k >= ls || k >= ld) throw Error(DOT_ERR_ARG, "need 0 <= k < min(ls, ld)");
+    std::vector<double> hW = host_copy(P, W, (size_t)P->n_src * ls, where);
+    std::vector<double> hV = host_copy(P, V, (size_t)P->n_det * ld, where);
+    DBuf<double2> t0, t1;
+    const double2* XU = get_fields(P, 0, {}, true, P->n_src, t0);
+    const double2* XL = get_fields(P, 1, {}, true, P->n_det, t1);
+    OptContext oc{P->arena, P->stream, P->n_freq, P->n_src, P->n_det, P->n_p, P->K, P->nP,
+                  XU, XL, P->d_S_slot.get(), P->d_G.get(), &P->stats.kernel_launches};
+    double obj = optimize_two_phase(oc, k, hW, ls, hV, ld);
+    if (objective_out) *objective_out = obj;
+    if (where == DOT_HOST) {
+        std::memcpy(W_out, hW.data(), hW.size() * sizeof(double));
+        std::memcpy(V_out, hV.data(), hV.size() * sizeof(double));
+    } else {
+        DOT_CUDA_TRY(cudaMemcpyAsync(W_out, hW.data(), hW.size() * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+        DOT_CUDA_TRY(cudaMemcpyAsync(V_out, hV.data(), hV.size() * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+        sync(P);
+    }
+    DOT_API_END(P)
+}
+
+int dot_absorption(dot_problem* P, double* mu_out, int where) {
+    DOT_API_BEGIN
+    if (!P || !mu_out) throw Error(DOT_ERR_ARG, "null argument");
+    require_params(P);
+    from_device(P, mu_out, P->d_mu.get(), P->N, where);
+    sync(P);
+    DOT_API_END(P)
+}
+
+int dot_support(dot_problem* P, int32_t* K_out, int64_t* nodes_out, double* G_out, int where) {
+    DOT_API_BEGIN
+    if (!P) throw Error(DOT_ERR_ARG, "null problem");
+    require_params(P);
+    if (K_out) *K_out = P->K;
+    if (nodes_out && P->K) {
+        std::vector<int32_t> h(P->K);
+        DOT_CUDA_TRY(cudaMemcpyAsync(h.data(), P->d_S.get(), P->K * sizeof(int32_t), cudaMemcpyDeviceToHost, P->stream));
+        sync(P);
+        std::vector<int64_t> h64(h.begin(), h.end());
+        if (where == DOT_HOST) std::memcpy(nodes_out, h64.data(), h64.size() * 8);
+        else DOT_CUDA_TRY(cudaMemcpyAsync(nodes_out, h64.data(), h64.size() * 8, cudaMemcpyHostToDevice, P->stream));
+    }
+    if (G_out && P->K) from_device(P, G_out, P->d_G.get(), (size_t)P->K * P->n_p, where);
+    sync(P);
+    DOT_API_END(P)
+}
+
+int dot_samples(dot_problem* P, int32_t* n_out, int64_t* nodes_out, int where) {
+    DOT_API_BEGIN
+    if (!P) throw Error(DOT_ERR_ARG, "null problem");
+    require_params(P);
+    if (n_out) *n_out = P->nP;
+    if (nodes_out && P->nP) {
+        std::vector<int32_t> h(P->nP);
+        DOT_CUDA_TRY(cudaMemcpyAsync(h.data(), P->d_P.get(), P->nP * sizeof(int32_t), cudaMemcpyDeviceToHost, P->stream));
+        sync(P);
+        std::vector<int64_t> h64(h.begin(), h.end());
+        if (where == DOT_HOST) std::memcpy(nodes_out, h64.data(), h64.size() * 8);
+        else DOT_CUDA_TRY(cudaMemcpyAsync(nodes_out, h64.data(), h64.size() * 8, cudaMemcpyHostToDevice, P->stream));
+        sync(P);
+    }
+    DOT_API_END(P)
+}
+
+int dot_apply(dot_problem* P, int32_t freq, int32_t nrhs, const double* u, double* Au, int where) {
+    DOT_API_BEGIN
+    if (!P || !u || !Au) throw Error(DOT_ERR_ARG, "null argument");
+    require_params(P);
+    if (freq < 0 || freq >= P->n_freq || nrhs < 1) throw Error(DOT_ERR_ARG, "bad freq / nrhs");
+    const size_t n = (size_t)nrhs * P->N;
+    DBuf<double2> du = to_device(P, reinterpret_cast<const double2*>(u), n, where);
+    DBuf<double2> dA(P->arena, n);
+    std::vector<double> sh(nrhs, P->omega[freq] / P->nu);
+    DBuf<double> dsh = to_device(P, sh.data(), sh.size(), DOT_HOST);
+    launch_apply(P->op, P->d_mu.get(), dsh.get(), du.get(), dA.get(), nrhs, P->stream);
+    P->stats.kernel_launches++;
+    from_device(P, reinterpret_cast<double2*>(Au), dA.get(), n, where);
+    sync(P);
+    DOT_API_END(P)
+}
+
+int dot_solve(dot_problem* P, int32_t nrhs, const int32_t* freq, const double* b, double* x, int where,
+              int32_t* iters_out) {
+    DOT_API_BEGIN
+    if (!P || !freq || !b || !x || nrhs < 1) throw Error(DOT_ERR_ARG, "bad argument");
+    require_params(P);
+    const size_t n = (size_t)nrhs * P->N;
+    DBuf<double2> db = to_device(P, reinterpret_cast<const double2*>(b), n, where);
+    DBuf<int32_t> df = to_device(P, freq, nrhs, where);
+    DBuf<double2> dx(P->arena, n);
+    auto it = solve_rhs(P, -1, nullptr, 1, nrhs, db.get(), df.get(), nullptr, dx.get());
+    from_device(P, reinterpret_cast<double2*>(x), dx.get(), n, where);
+    sync(P);
+    if (iters_out) std::copy(it.begin(), it.end(), iters_out);
+    DOT_API_END(P)
+}
+
+int dot_solve_sampled(dot_problem* P, int32_t side, const double* coeff, int32_t ncols, int where, double* X_out) {
+    DOT_API_BEGIN
+    if (!P || (side != 0 && side != 1)) throw Error(DOT_ERR_ARG, "bad argument");
+    require_params(P);
+    const int n_side = side == 0 ? P->n_src : P->n_det;
+    check_side_matrix(coeff, n_side, ncols, "coeff");
+    std::vector<double> hc = coeff ? host_copy(P, coeff, (size_t)n_side * ncols, where) : std::vector<double>();
+    DBuf<double2> tmp;
+    const double2* X = get_fields(P, side, hc, coeff == nullptr, ncols, tmp);
+    if (X_out) from_device(P, reinterpret_cast<double2*>(X_out), X, (size_t)P->n_freq * ncols * P->nP, where);
+    sync(P);
+    DOT_API_END(P)
+}
+
+int dot_contract(void* stream, int32_t nb, int32_t K, int32_t ld, int32_t ls, int32_t n_p, const double* Lam,
+                 const double* U, const double* G, double* J) {
+    try {
+        if (nb < 1 || K < 0 || ld < 1 || ls < 1 || n_p < 1 || n_p > 256 || !Lam || !U || !G || !J)
+            throw Error(DOT_ERR_ARG, "bad argument");
+        launch_contract(nb, K, ld, ls, n_p, reinterpret_cast<const double2*>(Lam), (size_t)ld * K,
+                        reinterpret_cast<const double2*>(U), (size_t)ls * K, G, reinterpret_cast<double2*>(J),
+                        static_cast<cudaStream_t>(stream));
+        return DOT_OK;
+    } catch (const Error& e) {
+        g_create_error = e.msg;
+        return e.code;
+    }
+}
+
+}  // extern "C"

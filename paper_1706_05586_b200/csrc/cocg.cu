@@ -1,0 +1,495 @@
+// Batched multi-RHS COCG for the complex-symmetric DOT operator A(omega, p)
+// (Eq. (2.1), Eq. (2.5); solves of Sec. 3.3.1 "we solve
+// A(p) z_i = B w_i ... A^T(p) y_j = C v_j").
+//
+// Single-pass COCG: the state carried between passes is
+// (r_k, p_{k-1}) plus per-RHS scalars.  Pass k forms p_k = r_k + beta_k p_{k-1},
+// q_k = A p_k, r_{k+1} = r_k - alpha_k q_k and, in the same sweep, the reductions
+// rho_{k+1} = r^T r, mu_{k+1} = r^T A r, nu_{k+1} = r^T q_k and the direct
+// sigma_k = p_k^T q_k.  The next pass takes beta_{k+1} = rho_{k+1}/rho_k,
+// sigma_{k+1} = mu_{k+1} + 2 beta nu_{k+1} + beta^2 sigma_k, alpha = rho/sigma.
+// HBM traffic per point and iteration: read r, p; write r, p = 64 B.
+#include "kernels.h"
+
+namespace dot {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block reduction of kNumPartials doubles; result valid in thread 0.
+__device__ void block_reduce_partials(double (&acc)[kNumPartials], double* scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int i = 0; i < kNumPartials; ++i) acc[i] = warp_sum(acc[i]);
+    if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < kNumPartials; ++i) scratch[warp * kNumPartials + i] = acc[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kNumPartials; ++i) {
+            double s = 0;
+            for (int w = 0; w < nw; ++w) s += scratch[w * kNumPartials + i];   // fixed order
+            acc[i] = s;
+        }
+    }
+}
+
+struct Scalars {
+    double2 alpha, beta;
+    int active;   // 0: exit
+};
+
+// Scalar recurrences at the start of pass k (identical in every CTA of one RHS).
+__device__ Scalars pass_scalars(const PassArgs& a, int rhs, int tile) {
+    const int ntiles = a.tl.ntiles;
+    const RhsState prev = a.st[(a.k + 1) & 1][rhs];
+    RhsState cur = prev;
+    Scalars sc;
+    sc.alpha = cmk(0, 0);
+    sc.beta = cmk(0, 0);
+    sc.active = 0;
+    if (!prev.done) {
+        const double* pp = a.part[a.k & 1] + (size_t)rhs * ntiles * kNumPartials;
+        double s[kNumPartials];
+        for (int i = 0; i < kNumPartials; ++i) s[i] = 0;
+        for (int t = 0; t < ntiles; ++t)
+            for (int i = 0; i < kNumPartials; ++i) s[i] += pp[t * kNumPartials + i];
+        const double2 rho = cmk(s[0], s[1]), mu = cmk(s[2], s[3]), nu = cmk(s[4], s[5]);
+        const double2 sigd = cmk(s[6], s[7]);
+        const double nrm2 = s[8];
+        if (a.k == 0) cur.bnorm2 = nrm2;
+        double2 beta = cmk(0, 0), sigma = mu;
+        if (a.k > 0) {
+            beta = cdiv(rho, cmk(prev.rho_re, prev.rho_im));
+            sigma = cadd(cadd(mu, cscale(cmul(beta, nu), 2.0)), cmul(cmul(beta, beta), sigd));
+        }
+        const double2 alpha = cdiv(rho, sigma);
+        if (!(nrm2 > a.tol2 * cur.bnorm2)) {           // converged (also b = 0)
+            cur.done = 1;
+            cur.iters = a.k;
+        } else if (a.k >= a.max_iter) {
+            cur.done = 1;
+            cur.iters = a.k;
+            cur.flag = DOT_ERR_NOCONV;
+        } else if (!isfinite(alpha.x) || !isfinite(alpha.y) || !isfinite(beta.x) ||
+                   !isfinite(beta.y)) {
+            cur.done = 1;
+            cur.iters = a.k;
+            cur.flag = DOT_ERR_BREAKDOWN;
+        } else {
+            sc.active = 1;
+            sc.alpha = alpha;
+            sc.beta = beta;
+            cur.rho_re = rho.x;
+            cur.rho_im = rho.y;
+            cur.alpha_re = alpha.x;
+            cur.alpha_im = alpha.y;
+        }
+    }
+    if (tile == 0) a.st[a.k & 1][rhs] = cur;
+    return sc;
+}
+
+// One fused COCG pass.  grid = (ntiles, nb), block = tl.threads.
+template <bool FULLX>
+__global__ void __launch_bounds__(512, 1) cocg_pass_kernel(const PassArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int tile = blockIdx.x, rhs = blockIdx.y;
+    const int nx = a.op.nx, ny = a.op.ny, nz = a.op.nz;
+    const int TY = a.tl.TY, NS = a.tl.nslots;
+    const int rowsP = TY + 4, rowsR = TY + 2;
+    const size_t N = (size_t)nx * ny * nz;
+    const int j0 = tile * TY;
+    const int ty_own = min(TY, ny - j0);
+
+    // ---- shared memory carve-up
+    double2* slotR = reinterpret_cast<double2*>(smem_raw);                 // [NS][rowsP][nx]
+    double2* slotP = slotR + (size_t)NS * rowsP * nx;                      // [NS][rowsP][nx]
+    double2* rn = slotP + (size_t)NS * rowsP * nx;                         // [3][rowsR][nx]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(rn + (size_t)3 * rowsR * nx);   // [NS]
+    double* scratch = reinterpret_cast<double*>(bars + NS);                // [16*9 + 8]
+    __shared__ Scalars sh_sc;
+
+    if (threadIdx.x == 0) sh_sc = pass_scalars(a, rhs, tile);
+    __syncthreads();
+    const Scalars sc = sh_sc;
+    if (!sc.active) return;
+    const double2 alpha = sc.alpha, beta = sc.beta;
+    const bool first = (a.k == 0);
+    const double shift = a.shift[rhs];
+    const int kin = a.k & 1, kout = kin ^ 1;
+    const double2* __restrict__ Rin = a.R[kin] + (size_t)rhs * N;
+    const double2* __restrict__ Pin = a.Pv[kin] + (size_t)rhs * N;
+    double2* __restrict__ Rout = a.R[kout] + (size_t)rhs * N;
+    double2* __restrict__ Pout = a.Pv[kout] + (size_t)rhs * N;
+
+    // rows of the tile window that lie in the domain: [jlo, jhi) global
+    const int jlo = max(j0 - 2, 0), jhi = min(j0 + TY + 2, ny);
+    const int row_off = jlo - (j0 - 2);
+    const uint32_t plane_bytes = (uint32_t)((jhi - jlo) * nx * sizeof(double2));
+
+    // zero the out-of-domain rows of all slots once (TMA never writes them)
+    for (int idx = threadIdx.x; idx < NS * rowsP * nx; idx += blockDim.x) {
+        int row = (idx / nx) % rowsP;
+        int jg = j0 - 2 + row;
+        if (jg < 0 || jg >= ny) {
+            slotR[idx] = cmk(0, 0);
+            slotP[idx] = cmk(0, 0);
+        }
+    }
+    for (int idx = threadIdx.x; idx < 3 * rowsR * nx; idx += blockDim.x) rn[idx] = cmk(0, 0);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const int PD = NS - 3;   // prefetch distance
+    auto issue = [&](int z) {
+        if (z >= nz) return;
+        const int s = z % NS;
+        fence_proxy_async();
+        const size_t g = ((size_t)z * ny + jlo) * nx;
+        const size_t o = ((size_t)s * rowsP + row_off) * nx;
+        mbar_expect_tx(&bars[s], first ? plane_bytes : 2 * plane_bytes);
+        bulk_g2s(slotR + o, Rin + g, plane_bytes, &bars[s]);
+        if (!first) bulk_g2s(slotP + o, Pin + g, plane_bytes, &bars[s]);
+    };
+    if (threadIdx.x == 0)
+        for (int z = 0; z < PD; ++z) issue(z);
+
+    double acc[kNumPartials];
+#pragma unroll
+    for (int i = 0; i < kNumPartials; ++i) acc[i] = 0;
+
+    const int32_t* soff = a.samp_off + (size_t)tile;
+    const double cx = a.op.cx, cy = a.op.cy, cz = a.op.cz;
+
+    for (int f = 0; f < nz + 2; ++f) {
+        // (1) prefetch plane f + PD (its slot held plane f - 3, released last step)
+        if (threadIdx.x == 0) issue(f + PD);
+        // (2) p_k(f) = r_k(f) + beta p_{k-1}(f), in place in slotP
+        if (f < nz) {
+            const int s = f % NS;
+            mbar_wait(&bars[s], (uint32_t)((f / NS) & 1));
+            double2* sp = slotP + (size_t)s * rowsP * nx;
+            const double2* sr = slotR + (size_t)s * rowsP * nx;
+            const int b0 = row_off * nx, b1 = (row_off + (jhi - jlo)) * nx;
+            for (int idx = b0 + threadIdx.x; idx < b1; idx += blockDim.x) {
+                double2 r = sr[idx];
+                sp[idx] = first ? r : cfma(beta, sp[idx], r);
+            }
+        }
+        __syncthreads();
+        // (3) plane g = f - 1: q = A p_k, r_{k+1} = r_k - alpha q  (rows -1 .. TY)
+        const int g = f - 1;
+        if (g >= 0 && g < nz) {
+            const int sg = g % NS;
+            const double2* pc = slotP + (size_t)sg * rowsP * nx;
+            const double2* pd = slotP + (size_t)((g + NS - 1) % NS) * rowsP * nx;   // plane g-1
+            const double2* pu = slotP + (size_t)((g + 1) % NS) * rowsP * nx;        // plane g+1
+            const double2* rc = slotR + (size_t)sg * rowsP * nx;
+            double2* rno = rn + (size_t)(g % 3) * rowsR * nx;
+            const double th = theta_of(g, nz);
+            const bool hasD = g > 0, hasU = g < nz - 1;
+            for (int idx = threadIdx.x; idx < rowsR * nx; idx += blockDim.x) {
+                const int lr = idx / nx, i = idx - lr * nx;   // lr = local row + 1
+                const int jg = j0 - 1 + lr;
+                if (jg < 0 || jg >= ny) continue;
+                const int sidx = (lr + 1) * nx + i;           // row in slot coords
+                const double2 p0 = pc[sidx];
+                double2 lat = cmk(0, 0);
+                if (i > 0) lat = cadd(lat, cscale(pc[sidx - 1], cx));
+                if (i < nx - 1) lat = cadd(lat, cscale(pc[sidx + 1], cx));
+                lat = cadd(lat, cscale(cadd(pc[sidx - nx], pc[sidx + nx]), cy));
+                double2 zz = cmk(0, 0);
+                if (hasD) zz = cadd(zz, pd[sidx]);
+                if (hasU) zz = cadd(zz, pu[sidx]);
+                const double mu = a.mu[((size_t)g * ny + jg) * nx + i];
+                const double2 dg = diag_of(a.op, g, mu, shift);
+                double2 q = cmul(dg, p0);
+                q = csub(q, cscale(lat, th));
+                q = csub(q, cscale(zz, cz));
+                const double2 rnew = csub(rc[sidx], cmul(alpha, q));
+                rno[idx] = rnew;
+                if (lr >= 1 && lr <= ty_own) {
+                    // nu += r_{k+1} q ; sigma_direct += p_k q   (bilinear)
+                    acc[4] = fma(rnew.x, q.x, fma(-rnew.y, q.y, acc[4]));
+                    acc[5] = fma(rnew.x, q.y, fma(rnew.y, q.x, acc[5]));
+                    acc[6] = fma(p0.x, q.x, fma(-p0.y, q.y, acc[6]));
+                    acc[7] = fma(p0.x, q.y, fma(p0.y, q.x, acc[7]));
+                }
+            }
+        }
+        __syncthreads();
+        // (4) plane t = f - 2: A r_{k+1}, reductions, write r_{k+1}, p_k, samples
+        const int t = f - 2;
+        if (t >= 0 && t < nz) {
+            const double2* rc = rn + (size_t)(t % 3) * rowsR * nx;
+            const double2* rd = rn + (size_t)((t + 2) % 3) * rowsR * nx;   // plane t-1
+            const double2* ru = rn + (size_t)((t + 1) % 3) * rowsR * nx;   // plane t+1
+            const double2* pt = slotP + (size_t)(t % NS) * rowsP * nx;
+            const double th = theta_of(t, nz);
+            const bool hasD = t > 0, hasU = t < nz - 1;
+            const size_t gbase = ((size_t)t * ny + j0) * nx;
+            for (int idx = threadIdx.x; idx < ty_own * nx; idx += blockDim.x) {
+                const int lr = idx / nx, i = idx - lr * nx;
+                const int ridx = (lr + 1) * nx + i;
+                const double2 r0 = rc[ridx];
+                double2 lat = cmk(0, 0);
+                if (i > 0) lat = cadd(lat, cscale(rc[ridx - 1], cx));
+                if (i < nx - 1) lat = cadd(lat, cscale(rc[ridx + 1], cx));
+                lat = cadd(lat, cscale(cadd(rc[ridx - nx], rc[ridx + nx]), cy));
+                double2 zz = cmk(0, 0);
+                if (hasD) zz = cadd(zz, rd[ridx]);
+                if (hasU) zz = cadd(zz, ru[ridx]);
+                const double mu = a.mu[gbase + idx];
+                const double2 dg = diag_of(a.op, t, mu, shift);
+                double2 ar = cmul(dg, r0);
+                ar = csub(ar, cscale(lat, th));
+                ar = csub(ar, cscale(zz, cz));
+                acc[0] = fma(r0.x, r0.x, fma(-r0.y, r0.y, acc[0]));
+                acc[1] = fma(2.0 * r0.x, r0.y, acc[1]);
+                acc[2] = fma(r0.x, ar.x, fma(-r0.y, ar.y, acc[2]));
+                acc[3] = fma(r0.x, ar.y, fma(r0.y, ar.x, acc[3]));
+                acc[8] = fma(r0.x, r0.x, fma(r0.y, r0.y, acc[8]));
+                const double2 pk = pt[(lr + 2) * nx + i];
+                Rout[gbase + idx] = r0;
+                Pout[gbase + idx] = pk;
+                if (FULLX) {
+                    double2* X = a.X + (size_t)rhs * N;
+                    X[gbase + idx] = cfma(alpha, pk, X[gbase + idx]);
+                }
+            }
+            if (!FULLX && a.nP > 0) {
+                const int s0 = soff[(size_t)t * a.tl.ntiles], s1 = soff[(size_t)t * a.tl.ntiles + 1];
+                double2* XP = a.XP + (size_t)rhs * a.nP;
+                for (int sidx = s0 + threadIdx.x; sidx < s1; sidx += blockDim.x) {
+                    const int node = a.samp_nodes[sidx];
+                    const int rem = node - t * nx * ny;
+                    const int jg = rem / nx, i = rem - jg * nx;
+                    const double2 pk = pt[(jg - j0 + 2) * nx + i];
+                    XP[sidx] = cfma(alpha, pk, XP[sidx]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    block_reduce_partials(acc, scratch);
+    if (threadIdx.x == 0) {
+        double* out = a.part[kout] + ((size_t)rhs * a.tl.ntiles + tile) * kNumPartials;
+        for (int i = 0; i < kNumPartials; ++i) out[i] = acc[i];
+    }
+}
+
+// (A u)(n) from global memory (reference-style stencil; used by init and dot_apply)
+__device__ __forceinline__ double2 apply_point(const OpConst& op, const double* mu, double shift,
+                                               const double2* u, int i, int j, int k) {
+    const int nx = op.nx, ny = op.ny, nz = op.nz;
+    const size_t n = ((size_t)k * ny + j) * nx + i;
+    const double2 u0 = u[n];
+    double2 lx = cmk(0, 0), ly = cmk(0, 0), lz = cmk(0, 0);
+    if (i > 0) lx = cadd(lx, u[n - 1]);
+    if (i < nx - 1) lx = cadd(lx, u[n + 1]);
+    if (j > 0) ly = cadd(ly, u[n - nx]);
+    if (j < ny - 1) ly = cadd(ly, u[n + nx]);
+    if (k > 0) lz = cadd(lz, u[n - (size_t)nx * ny]);
+    if (k < nz - 1) lz = cadd(lz, u[n + (size_t)nx * ny]);
+    const double th = theta_of(k, nz);
+    double2 r = cmul(diag_of(op, k, mu[n], shift), u0);
+    r = csub(r, cscale(cadd(cscale(lx, op.cx), cscale(ly, op.cy)), th));
+    r = csub(r, cscale(lz, op.cz));
+    return r;
+}
+
+// partials[0]: rho_0 = b^T b, mu_0 = b^T A b, |b|^2 (tile-owned rows, all planes)
+__global__ void __launch_bounds__(256) cocg_init_kernel(const PassArgs a) {
+    __shared__ double scratch[8 * kNumPartials];
+    const int tile = blockIdx.x, rhs = blockIdx.y;
+    const int nx = a.op.nx, ny = a.op.ny, nz = a.op.nz;
+    const size_t N = (size_t)nx * ny * nz;
+    const int j0 = tile * a.tl.TY, ty_own = min(a.tl.TY, ny - j0);
+    const double2* b = a.R[0] + (size_t)rhs * N;
+    const double shift = a.shift[rhs];
+    double acc[kNumPartials];
+    for (int i = 0; i < kNumPartials; ++i) acc[i] = 0;
+    const int per_plane = ty_own * nx;
+    for (int idx = threadIdx.x; idx < per_plane * nz; idx += blockDim.x) {
+        const int k = idx / per_plane, rem = idx - k * per_plane;
+        const int j = j0 + rem / nx, i = rem % nx;
+        const double2 r0 = b[((size_t)k * ny + j) * nx + i];
+        if (r0.x == 0.0 && r0.y == 0.0) continue;
+        const double2 ar = apply_point(a.op, a.mu, shift, b, i, j, k);
+        acc[0] = fma(r0.x, r0.x, fma(-r0.y, r0.y, acc[0]));
+        acc[1] = fma(2.0 * r0.x, r0.y, acc[1]);
+        acc[2] = fma(r0.x, ar.x, fma(-r0.y, ar.y, acc[2]));
+        acc[3] = fma(r0.x, ar.y, fma(r0.y, ar.x, acc[3]));
+        acc[8] = fma(r0.x, r0.x, fma(r0.y, r0.y, acc[8]));
+    }
+    block_reduce_partials(acc, scratch);
+    if (threadIdx.x == 0) {
+        double* out = a.part[0] + ((size_t)rhs * a.tl.ntiles + tile) * kNumPartials;
+        for (int i = 0; i < kNumPartials; ++i) out[i] = acc[i];
+    }
+    if (threadIdx.x == 0 && tile == 0) {
+        RhsState s{};
+        a.st[1][rhs] = s;     // pass 0 reads st[1]: not done
+    }
+}
+
+__global__ void apply_kernel(OpConst op, const double* mu, const double* shift, const double2* u,
+                             double2* Au, int nb) {
+    const size_t N = (size_t)op.nx * op.ny * op.nz;
+    const int rhs = blockIdx.y;
+    for (size_t n = blockIdx.x * (size_t)blockDim.x + threadIdx.x; n < N;
+         n += (size_t)gridDim.x * blockDim.x) {
+        const int i = n % op.nx, j = (n / op.nx) % op.ny, k = n / ((size_t)op.nx * op.ny);
+        Au[(size_t)rhs * N + n] = apply_point(op, mu, shift[rhs], u + (size_t)rhs * N, i, j, k);
+    }
+}
+
+__global__ void count_active_kernel(const RhsState* st, int nb, int* out) {
+    __shared__ int cnt;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    int c = 0;
+    for (int r = threadIdx.x; r < nb; r += blockDim.x) c += st[r].done ? 0 : 1;
+    atomicAdd(&cnt, c);
+    __syncthreads();
+    if (threadIdx.x == 0) *out = cnt;
+}
+
+__global__ void scatter_rhs_kernel(double2* R0, size_t N, long long rg0, int ncols, const int32_t* nodes,
+                                   int nnodes, const double* coeff, const double* scale) {
+    const int r = blockIdx.x;
+    const int c = (int)((rg0 + r) % ncols);
+    for (int a = threadIdx.x; a < nnodes; a += blockDim.x) {
+        const double w = coeff ? coeff[(size_t)a * ncols + c] : (a == c ? 1.0 : 0.0);
+        if (w != 0.0) R0[(size_t)r * N + nodes[a]] = cmk(w * scale[a], 0.0);
+    }
+}
+
+__global__ void fill_shift_kernel(double* shift, int nb, long long rg0, int ncols, const double* w) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nb; r += gridDim.x * blockDim.x)
+        shift[r] = w[(rg0 + r) / ncols];
+}
+
+}  // namespace
+
+CocgTiling cocg_tiling(int nx, int ny, int nz) {
+    CocgTiling t;
+    const size_t budget = 220 * 1024;
+    const size_t row = (size_t)nx * sizeof(double2);
+    auto smem_of = [&](int TY, int NS) {
+        return (size_t)NS * 2 * (TY + 4) * row + 3 * (TY + 2) * row + NS * 8 + (16 * kNumPartials + 8) * 8 + 256;
+    };
+    int best = 0, bestNS = 4;
+    for (int NS = 5; NS >= 4; --NS) {
+        int TY = 0;
+        for (int ty = 1; ty <= ny; ++ty)
+            if (smem_of(ty, NS) <= budget) TY = ty;
+        if (NS == 5 && TY >= 12) { best = TY; bestNS = 5; break; }
+        if (NS == 4) { best = TY; bestNS = 4; }
+    }
+    if (best <= 0) throw Error(DOT_ERR_ARG, "grid rows too long for the shared-memory plane ring (nx too large)");
+    // balance tiles: same count, smaller rows
+    int ntiles = (ny + best - 1) / best;
+    int TY = (ny + ntiles - 1) / ntiles;
+    t.TY = TY;
+    t.ntiles = ntiles;
+    t.nslots = bestNS;
+    t.threads = 512;
+    t.smem = smem_of(TY, bestNS);
+    return t;
+}
+
+void launch_cocg_init(const PassArgs& a, int nb, cudaStream_t s) {
+    dim3 grid(a.tl.ntiles, nb);
+    cocg_init_kernel<<<grid, 256, 0, s>>>(a);
+    DOT_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_cocg_pass(const PassArgs& a, int nb, cudaStream_t s) {
+    dim3 grid(a.tl.ntiles, nb);
+    if (a.X) {
+        static bool attr = false;
+        if (!attr) {
+            DOT_CUDA_TRY(cudaFuncSetAttribute(cocg_pass_kernel<true>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            attr = true;
+        }
+        cocg_pass_kernel<true><<<grid, a.tl.threads, a.tl.smem, s>>>(a);
+    } else {
+        static bool attr = false;
+        if (!attr) {
+            DOT_CUDA_TRY(cudaFuncSetAttribute(cocg_pass_kernel<false>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            attr = true;
+        }
+        cocg_pass_kernel<false><<<grid, a.tl.threads, a.tl.smem, s>>>(a);
+    }
+    DOT_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_count_active(const RhsState* st, int nb, int* d_count, cudaStream_t s) {
+    count_active_kernel<<<1, 256, 0, s>>>(st, nb, d_count);
+    DOT_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_apply(const OpConst& op, const double* mu, const double* shift, const double2* u,
+                  double2* Au, int nb, cudaStream_t s) {
+    const size_t N = (size_t)op.nx * op.ny * op.nz;
+    dim3 grid((unsigned)std::min<size_t>((N + 255) / 256, 4096), nb);
+    apply_kernel<<<grid, 256, 0, s>>>(op, mu, shift, u, Au, nb);
+    DOT_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_scatter_rhs(double2* R0, size_t N, int nb, long long rg0, int ncols, const int32_t* nodes,
+                        int nnodes, const double* coeff, const double* scale, cudaStream_t s) {
+    scatter_rhs_kernel<<<nb, 256, 0, s>>>(R0, N, rg0, ncols, nodes, nnodes, coeff, scale);
+    DOT_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_fill_shift(double* shift, int nb, long long rg0, int ncols, const double* omega_over_nu,
+                       cudaStream_t s) {
+    fill_shift_kernel<<<(nb + 255) / 256, 256, 0, s>>>(shift, nb, rg0, ncols, omega_over_nu);
+    DOT_CUDA_TRY(cudaGetLastError());
+}
+
+}  // namespace dot

@@ -1,0 +1,92 @@
+// Kernel launchers of the B200 DOT library (internal interface between the
+// C-ABI layer abi.cu and the kernel translation units).
+#pragma once
+#include "dot_common.cuh"
+
+namespace dot {
+
+// ------------------------------------------------------------------ cocg.cu
+// Tiling of the fused COCG pass: a CTA owns TY full x-rows of one RHS and
+// marches all nz planes; planes (with a 2-row y halo) are staged by TMA bulk
+// copies into a ring of `nslots` shared-memory slots.
+struct CocgTiling {
+    int TY = 0, ntiles = 0, nslots = 0, threads = 512;
+    size_t smem = 0;
+};
+CocgTiling cocg_tiling(int nx, int ny, int nz);
+
+struct PassArgs {
+    OpConst op;
+    CocgTiling tl;
+    int k = 0;                    // pass index
+    int max_iter = 0;
+    double tol2 = 0;              // tol^2
+    const double* mu = nullptr;   // [N] absorption
+    const double* shift = nullptr;// [nb] omega/nu of each RHS
+    double2* R[2] = {nullptr, nullptr};   // [nb][N] residual r (ping-pong)
+    double2* Pv[2] = {nullptr, nullptr};  // [nb][N] direction p (ping-pong)
+    double* part[2] = {nullptr, nullptr}; // [nb][ntiles][kNumPartials]
+    RhsState* st[2] = {nullptr, nullptr}; // [nb]
+    const int32_t* samp_nodes = nullptr;  // [nP] ascending node ids
+    const int32_t* samp_off = nullptr;    // [nz*ntiles+1] ranges of samples per (plane, tile)
+    double2* XP = nullptr;                // [nb][nP] sampled solution
+    int nP = 0;
+    double2* X = nullptr;                 // [nb][N] full solution (test mode) or null
+};
+
+void launch_cocg_init(const PassArgs& a, int nb, cudaStream_t s);
+void launch_cocg_pass(const PassArgs& a, int nb, cudaStream_t s);
+void launch_count_active(const RhsState* st, int nb, int* d_count, cudaStream_t s);
+void launch_apply(const OpConst& op, const double* mu, const double* shift, const double2* u,
+                  double2* Au, int nb, cudaStream_t s);
+// Chunk of the global RHS list r = f*ncols + c (r = rg0 .. rg0+nb-1):
+// R0[r][node[a]] = coeff[a*ncols + c] * scale[a]  (coeff == null: identity)
+void launch_scatter_rhs(double2* R0, size_t N, int nb, long long rg0, int ncols, const int32_t* nodes,
+                        int nnodes, const double* coeff, const double* scale, cudaStream_t s);
+// shift[r] = omega_over_nu[(rg0 + r) / ncols]
+void launch_fill_shift(double* shift, int nb, long long rg0, int ncols, const double* omega_over_nu,
+                       cudaStream_t s);
+
+// ------------------------------------------------------------------ pals.cu
+struct PalsConst {
+    int nx, ny, nz, n_rbf;
+    double hx, hy, hz, gamma, eps, cutoff, mua_in, mua_out;
+};
+// mu[N], flagS[N] (1 where dH/dphi != 0), flagP[N] = flagS | detector
+void launch_pals_eval(const PalsConst& c, const double* params, double* mu, int32_t* flagS,
+                      int32_t* flagP, cudaStream_t s);
+void launch_mark_nodes(int32_t* flag, const int32_t* nodes, int n, cudaStream_t s);
+// exclusive scan of int32 flags -> pos (int32), total -> *d_total
+size_t scan_temp_bytes(size_t n);
+void launch_exclusive_scan(const int32_t* in, int32_t* out, size_t n, int32_t* d_total, void* temp,
+                           cudaStream_t s);
+void launch_compact(const int32_t* flag, const int32_t* pos, size_t n, int32_t* out_nodes,
+                    cudaStream_t s);
+void launch_gather_rank(const int32_t* pos, const int32_t* nodes, int n, int32_t* out, cudaStream_t s);
+// G[s][k] = theta dmu/dp_k at S[s]
+void launch_pals_grad(const PalsConst& c, const double* params, const int32_t* S, int K, double* G,
+                      cudaStream_t s);
+void launch_sample_offsets(const int32_t* P, int nP, int nx, int ny, int nz, int TY, int ntiles,
+                           int32_t* off, cudaStream_t s);
+
+// ------------------------------------------------------------------ contract.cu
+void launch_contract(int nb, int K, int ld, int ls, int n_p, const double2* Lam, size_t lam_bstride,
+                     const double2* U, size_t u_bstride, const double* G, double2* J,
+                     cudaStream_t s);
+
+// ------------------------------------------------------------------ smallops.cu
+// out[b][m][n] = sum_k Rm[k*ldr + m] * Cx[b*sb + k*sk + n*sn]   (real^T x complex)
+void launch_rc_gemm(int nb, int M, int N, int K, const double* Rm, int ldr, const double2* Cx,
+                    size_t sb, size_t sk, size_t sn, double2* out, size_t ob, size_t om, size_t on,
+                    cudaStream_t s);
+// out[b][i][j] = X[b][i][idx[j]] (gather columns)
+void launch_gather_cols(int nb, int rows, int ncols, const double2* X, size_t xb, size_t xr,
+                        const int32_t* idx, double2* out, size_t ob, size_t orow, cudaStream_t s);
+// a[i] -= b[i] (complex)
+void launch_csub_inplace(double2* a, const double2* b, size_t n, cudaStream_t s);
+// *out = sum |a[i]|^2 (deterministic, single launch)
+void launch_sumsq(const double2* a, size_t n, double* out, cudaStream_t s);
+// x[i] *= 1 (real diagonal weights): y[b][i] = x[b][i] * w[i]
+void launch_transpose_data(const double2* D, int nf, int nd, int ns, double2* Dt, cudaStream_t s);
+
+}  // namespace dot
