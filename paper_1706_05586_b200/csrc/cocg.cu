@@ -447,23 +447,21 @@ void launch_cocg_init(const PassArgs& a, int nb, cudaStream_t s) {
 
 void launch_cocg_pass(const PassArgs& a, int nb, cudaStream_t s) {
     dim3 grid(a.tl.ntiles, nb);
-    if (a.X) {
-        static bool attr = false;
-        if (!attr) {
-            DOT_CUDA_TRY(cudaFuncSetAttribute(cocg_pass_kernel<true>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-            attr = true;
-        }
-        cocg_pass_kernel<true><<<grid, a.tl.threads, a.tl.smem, s>>>(a);
-    } else {
-        static bool attr = false;
-        if (!attr) {
-            DOT_CUDA_TRY(cudaFuncSetAttribute(cocg_pass_kernel<false>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-            attr = true;
-        }
-        cocg_pass_kernel<false><<<grid, a.tl.threads, a.tl.smem, s>>>(a);
+    static size_t attr_set[2] = {0, 0};
+    const int which = a.X ? 1 : 0;
+    if (attr_set[which] < a.tl.smem) {
+        if (which)
+            DOT_CUDA_TRY(cudaFuncSetAttribute(cocg_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)a.tl.smem));
+        else
+            DOT_CUDA_TRY(cudaFuncSetAttribute(cocg_pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)a.tl.smem));
+        attr_set[which] = a.tl.smem;
     }
+    if (which)
+        cocg_pass_kernel<true><<<grid, a.tl.threads, a.tl.smem, s>>>(a);
+    else
+        cocg_pass_kernel<false><<<grid, a.tl.threads, a.tl.smem, s>>>(a);
     DOT_CUDA_TRY(cudaGetLastError());
 }
 
