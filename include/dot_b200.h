@@ -177,6 +177,13 @@ int dot_solve(dot_problem* P, int32_t nrhs, const int32_t* freq, const double* b
  * solution on the sample nodes P (dot_samples), solved fields are cached. */
 int dot_solve_sampled(dot_problem* P, int32_t side, const double* coeff, int32_t ncols,
                       int where, double* X_out);
+/* Same fields restricted to the support S of dA/dp (the Jacobian's only
+ * consumers, L972): out [n_freq][ncols][K] complex, K = |S| in dot_support
+ * order.  Fields of combinations of already-solved point sources (identity or
+ * selection caches) are formed by linear combination without new solves;
+ * multi-GPU callers all-reduce these partial combinations. */
+int dot_fields_on_support(dot_problem* P, int32_t side, const double* coeff, int32_t ncols, int where,
+                          double* out);
 /* Sample nodes P = S u detectors u sources (ascending, [n_samples] int64). */
 int dot_samples(dot_problem* P, int32_t* n_out, int64_t* nodes_out, int where);
 

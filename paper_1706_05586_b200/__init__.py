@@ -202,6 +202,33 @@ class DOTProblem:
                                               C.c_void_p(G.ctypes.data), DOT_HOST))
         return nodes, G
 
+    def support_weights(self):
+        """G on the support as a CUDA tensor [K][n_p] (device copy, no host trip)."""
+        import torch
+        K = C.c_int32()
+        self._check(self._lib.dot_support(self._h, C.byref(K), None, None, DOT_DEVICE))
+        G = torch.empty((K.value, self.n_p), dtype=torch.float64, device="cuda")
+        if K.value:
+            self._check(self._lib.dot_support(self._h, C.byref(K), None, C.c_void_p(G.data_ptr()), DOT_DEVICE))
+        return G
+
+    def fields_on_support(self, side, coeff=None, where=None):
+        """Fields of B coeff (side 0) / C coeff (side 1) on the support S:
+        [n_freq][ncols][K] complex (cached solves reused / combined)."""
+        n_side = self.n_src if side == 0 else self.n_det
+        ncols = n_side if coeff is None else int(coeff.shape[1])
+        K = C.c_int32()
+        self._check(self._lib.dot_support(self._h, C.byref(K), None, None, DOT_HOST))
+        a = _Args(where if where is not None else _where_of(coeff))
+        X, xp = a.out((self.n_freq, ncols, K.value), np.complex128)
+        self._check(self._lib.dot_fields_on_support(self._h, int(side), a.ptr(coeff, np.float64), ncols, a.where,
+                                                    xp))
+        return X
+
+    def contract(self, Lam, U, G):
+        """DMMA contraction on this problem's stream (see module-level contract)."""
+        return contract(Lam, U, G, stream=self.stream)
+
     def samples(self):
         n = C.c_int32()
         self._check(self._lib.dot_samples(self._h, C.byref(n), None, DOT_HOST))

@@ -21,6 +21,7 @@ struct FieldCache {
     bool identity = false;
     int ncols = 0;
     std::vector<double> coeff;        // [n_side][ncols] host copy (empty for identity)
+    std::vector<int> sel;             // cached columns are the point sources sel[j] (selection / identity)
     DBuf<double2> X;                  // [n_freq][ncols][nP]
 };
 
@@ -271,14 +272,29 @@ const double2* get_fields(dot_problem* P, int side, const std::vector<double>& h
     if (c.valid) {
         if (identity && c.identity) return c.X.get();
         if (!identity && !c.identity && c.ncols == ncols && c.coeff == hc) return c.X.get();
-        if (!identity && c.identity) {
-            // linear combination of cached full-data fields: X'[f][c][q] = sum_a coeff[a][c] X[f][a][q]
-            DBuf<double> dc = to_device(P, hc.data(), hc.size(), DOT_HOST);
-            tmp = DBuf<double2>(P->arena, (size_t)P->n_freq * ncols * std::max(P->nP, 1));
-            launch_rc_gemm(P->n_freq, ncols, P->nP, n_side, dc.get(), ncols, c.X.get(), (size_t)n_side * P->nP,
-                           P->nP, 1, tmp.get(), (size_t)ncols * P->nP, P->nP, 1, P->stream);
-            P->stats.kernel_launches++;
-            return tmp.get();
+        if (!identity && !c.sel.empty()) {
+            // The cache holds the fields of the point sources sel[0..m) (a selection /
+            // identity matrix).  If the request only combines those sources, form it by
+            // linear combination (no solves): X'[f][c][q] = sum_j coeff[sel_j][c] X[f][j][q].
+            const int m = (int)c.sel.size();
+            std::vector<char> in_sel(n_side, 0);
+            for (int j = 0; j < m; ++j) in_sel[c.sel[j]] = 1;
+            bool ok = true;
+            for (int a = 0; a < n_side && ok; ++a)
+                if (!in_sel[a])
+                    for (int q = 0; q < ncols; ++q)
+                        if (hc[(size_t)a * ncols + q] != 0.0) { ok = false; break; }
+            if (ok) {
+                std::vector<double> X((size_t)m * ncols);
+                for (int j = 0; j < m; ++j)
+                    for (int q = 0; q < ncols; ++q) X[(size_t)j * ncols + q] = hc[(size_t)c.sel[j] * ncols + q];
+                DBuf<double> dc = to_device(P, X.data(), X.size(), DOT_HOST);
+                tmp = DBuf<double2>(P->arena, (size_t)P->n_freq * ncols * std::max(P->nP, 1));
+                launch_rc_gemm(P->n_freq, ncols, P->nP, m, dc.get(), ncols, c.X.get(), (size_t)m * P->nP, P->nP, 1,
+                               tmp.get(), (size_t)ncols * P->nP, P->nP, 1, P->stream);
+                P->stats.kernel_launches++;
+                return tmp.get();
+            }
         }
     }
     // solve and cache
@@ -293,6 +309,23 @@ const double2* get_fields(dot_problem* P, int side, const std::vector<double>& h
     c.identity = identity;
     c.ncols = ncols;
     c.coeff = identity ? std::vector<double>() : hc;
+    c.sel.clear();
+    if (identity) {
+        for (int a = 0; a < n_side; ++a) c.sel.push_back(a);
+    } else {
+        // selection matrix? every column a unit vector e_a
+        bool is_sel = true;
+        std::vector<int> sel(ncols, -1);
+        for (int q = 0; q < ncols && is_sel; ++q)
+            for (int a = 0; a < n_side; ++a) {
+                const double v = hc[(size_t)a * ncols + q];
+                if (v == 0.0) continue;
+                if (v != 1.0 || sel[q] >= 0) { is_sel = false; break; }
+                sel[q] = a;
+            }
+        for (int q = 0; q < ncols && is_sel; ++q) is_sel = sel[q] >= 0;
+        if (is_sel) c.sel = sel;
+    }
     return c.X.get();
 }
 
@@ -301,6 +334,7 @@ void invalidate_caches(dot_problem* P) {
         c.valid = false;
         c.X.reset();
         c.coeff.clear();
+        c.sel.clear();
     }
 }
 
@@ -741,6 +775,33 @@ int dot_solve_sampled(dot_problem* P, int32_t side, const double* coeff, int32_t
     DBuf<double2> tmp;
     const double2* X = get_fields(P, side, hc, coeff == nullptr, ncols, tmp);
     if (X_out) from_device(P, reinterpret_cast<double2*>(X_out), X, (size_t)P->n_freq * ncols * P->nP, where);
+    sync(P);
+    DOT_API_END(P)
+}
+
+int dot_fields_on_support(dot_problem* P, int32_t side, const double* coeff, int32_t ncols, int where,
+                          double* out) {
+    DOT_API_BEGIN
+    if (!P || (side != 0 && side != 1) || !out) throw Error(DOT_ERR_ARG, "bad argument");
+    require_params(P);
+    const int n_side = side == 0 ? P->n_src : P->n_det;
+    check_side_matrix(coeff, n_side, ncols, "coeff");
+    std::vector<double> hc = coeff ? host_copy(P, coeff, (size_t)n_side * ncols, where) : std::vector<double>();
+    DBuf<double2> tmp;
+    const double2* X = get_fields(P, side, hc, coeff == nullptr, ncols, tmp);
+    const size_t n = (size_t)P->n_freq * ncols * P->K;
+    if (n) {
+        DBuf<double2> g;
+        double2* dst = reinterpret_cast<double2*>(out);
+        if (where == DOT_HOST) {
+            g = DBuf<double2>(P->arena, n);
+            dst = g.get();
+        }
+        launch_gather_cols(P->n_freq, ncols, P->K, X, (size_t)ncols * P->nP, P->nP, P->d_S_slot.get(), dst,
+                           (size_t)ncols * P->K, P->K, P->stream);
+        P->stats.kernel_launches++;
+        if (where == DOT_HOST) from_device(P, reinterpret_cast<double2*>(out), g.get(), n, where);
+    }
     sync(P);
     DOT_API_END(P)
 }
