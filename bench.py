@@ -218,7 +218,7 @@ def main():
     from paper_1706_05586_b200.sharded import ShardPlan, make_problem_for_rank, sharded_step
     plan = ShardPlan(rank, world, cfg.n_s, cfg.n_d)
     gp = make_problem_for_rank(dot, cfg, wl, plan)
-    gp.set_params(wl.p_true)
+    gp.set_params(wl.p_true_padded)
     X = gp.solve_sampled(0)
     samp = gp.samples()
     M = np.transpose(X[:, :, np.searchsorted(samp, wl.det_nodes)], (0, 2, 1))

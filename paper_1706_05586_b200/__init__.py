@@ -138,6 +138,8 @@ class DOTProblem:
         self._check(self._lib.dot_set_data(self._h, a.ptr(data, np.complex128), a.where))
 
     def set_params(self, p):
+        if int(np.prod(p.shape)) != self.n_p:
+            raise ValueError(f"p has {int(np.prod(p.shape))} entries, the problem has n_p = {self.n_p}")
         a = _Args(_where_of(p))
         self._check(self._lib.dot_set_params(self._h, a.ptr(p, np.float64), a.where))
 

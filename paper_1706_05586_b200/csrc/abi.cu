@@ -248,7 +248,9 @@ std::vector<int32_t> solve_rhs(dot_problem* P, int side, const double* d_coeff, 
             if (hs[r].flag == DOT_ERR_NOCONV)
                 throw Error(DOT_ERR_NOCONV, "COCG did not converge within max_iter for rhs " + std::to_string(r0 + r));
             if (hs[r].flag == DOT_ERR_BREAKDOWN)
-                throw Error(DOT_ERR_BREAKDOWN, "COCG breakdown for rhs " + std::to_string(r0 + r));
+                throw Error(DOT_ERR_BREAKDOWN, "COCG breakdown for rhs " + std::to_string(r0 + r) + " at iteration " +
+                                                   std::to_string(hs[r].iters) + " (batch of " + std::to_string(nb) +
+                                                   ", chunk start " + std::to_string(r0) + ")");
             iters[r0 + r] = hs[r].iters;
             mx = std::max(mx, hs[r].iters);
             mn = std::min(mn, hs[r].iters);

@@ -73,6 +73,14 @@ class Workload:
     xi: np.ndarray               # (n_freq, n_d, n_s) complex noise draws
 
     @property
+    def p_true_padded(self):
+        """p_true extended to n_rbf bases with zero-amplitude (alpha = 0) entries, so
+        a problem built for the current iterate's n_p can simulate the data."""
+        extra = self.cfg.n_rbf - self.p_true.size // 5
+        pad = np.tile(np.array([0.0, 1.0, 0.0, 0.0, 0.0]), max(extra, 0))
+        return np.concatenate([self.p_true, pad])
+
+    @property
     def W_or_I(self):
         return np.eye(self.cfg.n_s) if self.W is None else self.W
 
