@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -418,7 +419,14 @@ int dot_create(const dot_config* cfg, dot_problem** out) {
         P->op.cy = P->D / (P->hy * P->hy);
         P->op.cz = P->D / (P->hz * P->hz);
         P->op.robin = 1.0 / (2.0 * P->hz);
-        P->tl = cocg_tiling(P->nx, P->ny, P->nz);
+        {
+            // tuning knobs: planes prefetched, smem budget per CTA
+            const char* ePD = std::getenv("DOT_COCG_PREFETCH");
+            const char* eSM = std::getenv("DOT_COCG_SMEM_KB");
+            const int pd = ePD ? std::max(1, std::atoi(ePD)) : 1;
+            const size_t sm = eSM ? (size_t)std::atoi(eSM) * 1024 : 0;
+            P->tl = cocg_tiling(P->nx, P->ny, P->nz, pd, sm);
+        }
         P->pc = PalsConst{P->nx, P->ny, P->nz, P->n_rbf, P->hx, P->hy, P->hz, P->gamma, P->eps, P->cutoff,
                           P->mua_in, P->mua_out};
         DOT_CUDA_TRY(cudaMallocHost(&P->h_count, sizeof(int)));

@@ -127,23 +127,33 @@ __device__ Scalars pass_scalars(const PassArgs& a, int rhs, int tile) {
 }
 
 // One fused COCG pass.  grid = (ntiles, nb), block = tl.threads.
+// Shared memory: NS plane slots for r_k and p_{k-1} -> p_k ([TY+4 rows][nx+2] with zero
+// guard columns = Dirichlet x-faces, zero rows outside the y-range), and a ring of 3
+// r_{k+1} planes ([TY+2][nx+2]).  Step f of the z-march:
+//   A  issue bulk copies of plane f+PD                        (warp 0)
+//   B  p_k(f) = r_k(f) + beta p_{k-1}(f); write p_k(f) rows    (phase 1)
+//      A r_{k+1} at plane f-3, reductions, write r_{k+1}(f-3)  (phase 3)
+//   -- barrier --
+//   C  q = A p_k at plane f-1, r_{k+1}(f-1) = r_k - alpha q, reductions, samples
+//   -- barrier --
 template <bool FULLX>
 __global__ void __launch_bounds__(512, 1) cocg_pass_kernel(const PassArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int MAXR = 4;                       // rows per thread per phase (tiling guarantees)
     const int tile = blockIdx.x, rhs = blockIdx.y;
     const int nx = a.op.nx, ny = a.op.ny, nz = a.op.nz;
-    const int TY = a.tl.TY, NS = a.tl.nslots;
+    const int TY = a.tl.TY, NS = a.tl.nslots, RPT = a.tl.rpt;
+    const int W = nx + 2;                          // padded row stride
     const int rowsP = TY + 4, rowsR = TY + 2;
     const size_t N = (size_t)nx * ny * nz;
     const int j0 = tile * TY;
     const int ty_own = min(TY, ny - j0);
 
-    // ---- shared memory carve-up
-    double2* slotR = reinterpret_cast<double2*>(smem_raw);                 // [NS][rowsP][nx]
-    double2* slotP = slotR + (size_t)NS * rowsP * nx;                      // [NS][rowsP][nx]
-    double2* rn = slotP + (size_t)NS * rowsP * nx;                         // [3][rowsR][nx]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(rn + (size_t)3 * rowsR * nx);   // [NS]
-    double* scratch = reinterpret_cast<double*>(bars + NS);                // [16*9 + 8]
+    double2* slotR = reinterpret_cast<double2*>(smem_raw);                 // [NS][rowsP][W]
+    double2* slotP = slotR + (size_t)NS * rowsP * W;                        // [NS][rowsP][W]
+    double2* rn = slotP + (size_t)NS * rowsP * W;                           // [3][rowsR][W]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(rn + (size_t)3 * rowsR * W);
+    double* scratch = reinterpret_cast<double*>(bars + NS);
     __shared__ Scalars sh_sc;
 
     if (threadIdx.x == 0) sh_sc = pass_scalars(a, rhs, tile);
@@ -158,154 +168,170 @@ __global__ void __launch_bounds__(512, 1) cocg_pass_kernel(const PassArgs a) {
     const double2* __restrict__ Pin = a.Pv[kin] + (size_t)rhs * N;
     double2* __restrict__ Rout = a.R[kout] + (size_t)rhs * N;
     double2* __restrict__ Pout = a.Pv[kout] + (size_t)rhs * N;
+    const double* __restrict__ mu = a.mu;
 
-    // rows of the tile window that lie in the domain: [jlo, jhi) global
-    const int jlo = max(j0 - 2, 0), jhi = min(j0 + TY + 2, ny);
-    const int row_off = jlo - (j0 - 2);
-    const uint32_t plane_bytes = (uint32_t)((jhi - jlo) * nx * sizeof(double2));
+    // slot rows holding in-domain grid rows: [rlo, rhi); grid row of slot row r = j0 - 2 + r
+    const int rlo = max(0, 2 - j0), rhi = min(rowsP, ny - j0 + 2);
+    const uint32_t row_bytes = (uint32_t)(nx * sizeof(double2));
+    const uint32_t plane_bytes = (uint32_t)(rhi - rlo) * row_bytes;
 
-    // zero the out-of-domain rows of all slots once (TMA never writes them)
-    for (int idx = threadIdx.x; idx < NS * rowsP * nx; idx += blockDim.x) {
-        int row = (idx / nx) % rowsP;
-        int jg = j0 - 2 + row;
-        if (jg < 0 || jg >= ny) {
-            slotR[idx] = cmk(0, 0);
-            slotP[idx] = cmk(0, 0);
-        }
+    for (int idx = threadIdx.x; idx < NS * rowsP * W; idx += blockDim.x) {
+        slotR[idx] = cmk(0, 0);
+        slotP[idx] = cmk(0, 0);
     }
-    for (int idx = threadIdx.x; idx < 3 * rowsR * nx; idx += blockDim.x) rn[idx] = cmk(0, 0);
+    for (int idx = threadIdx.x; idx < 3 * rowsR * W; idx += blockDim.x) rn[idx] = cmk(0, 0);
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
-    const int PD = NS - 3;   // prefetch distance
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int PD = NS - 3;
+    // warp 0: lane 0 arms the barrier, then the lanes issue one bulk copy per row
     auto issue = [&](int z) {
-        if (z >= nz) return;
         const int s = z % NS;
-        fence_proxy_async();
-        const size_t g = ((size_t)z * ny + jlo) * nx;
-        const size_t o = ((size_t)s * rowsP + row_off) * nx;
-        mbar_expect_tx(&bars[s], first ? plane_bytes : 2 * plane_bytes);
-        bulk_g2s(slotR + o, Rin + g, plane_bytes, &bars[s]);
-        if (!first) bulk_g2s(slotP + o, Pin + g, plane_bytes, &bars[s]);
+        if (lane == 0) {
+            fence_proxy_async();
+            mbar_expect_tx(&bars[s], first ? plane_bytes : 2 * plane_bytes);
+        }
+        __syncwarp();
+        for (int r = rlo + lane; r < rhi; r += 32) {
+            const size_t g = ((size_t)z * ny + (j0 - 2 + r)) * nx;
+            const size_t o = ((size_t)s * rowsP + r) * W + 1;
+            bulk_g2s(slotR + o, Rin + g, row_bytes, &bars[s]);
+            if (!first) bulk_g2s(slotP + o, Pin + g, row_bytes, &bars[s]);
+        }
     };
-    if (threadIdx.x == 0)
-        for (int z = 0; z < PD; ++z) issue(z);
+    if (warp == 0)
+        for (int z = 0; z < PD && z < nz; ++z) issue(z);
+
+    const bool act = threadIdx.x < nx * RPT;
+    const int ci = act ? threadIdx.x % nx : 0;       // my column
+    const int rl = act ? threadIdx.x / nx : RPT;     // my first row within a sweep
+    const double cx = a.op.cx, cy = a.op.cy, cz = a.op.cz;
+    const double dbase = 2.0 * cx + 2.0 * cy;
+    const int32_t* soff = a.samp_off + (size_t)tile;
 
     double acc[kNumPartials];
 #pragma unroll
-    for (int i = 0; i < kNumPartials; ++i) acc[i] = 0;
+    for (int q = 0; q < kNumPartials; ++q) acc[q] = 0;
 
-    const int32_t* soff = a.samp_off + (size_t)tile;
-    const double cx = a.op.cx, cy = a.op.cy, cz = a.op.cz;
-
-    for (int f = 0; f < nz + 2; ++f) {
-        // (1) prefetch plane f + PD (its slot held plane f - 3, released last step)
-        if (threadIdx.x == 0) issue(f + PD);
-        // (2) p_k(f) = r_k(f) + beta p_{k-1}(f), in place in slotP
+    for (int f = 0; f < nz + 3; ++f) {
+        if (warp == 0 && f + PD < nz) issue(f + PD);
+        const int g = f - 1, t = f - 3;
+        // ---- prefetch mu for phase 3 (plane t, owned rows) and phase C (plane g, rows 1..TY+2)
+        double mu3[MAXR], mu2[MAXR];
+#pragma unroll
+        for (int m = 0; m < MAXR; ++m) {
+            const int r3 = rl + m * RPT;                         // owned row offset
+            mu3[m] = (t >= 0 && t < nz && r3 < ty_own) ? mu[((size_t)t * ny + j0 + r3) * nx + ci] : 0.0;
+            const int r2 = 1 + rl + m * RPT;                     // slot row
+            const int jg = j0 - 2 + r2;
+            mu2[m] = (g >= 0 && g < nz && r2 <= TY + 2 && jg >= 0 && jg < ny)
+                         ? mu[((size_t)g * ny + jg) * nx + ci] : 0.0;
+        }
+        // ---- B1: phase 1, plane f
         if (f < nz) {
             const int s = f % NS;
             mbar_wait(&bars[s], (uint32_t)((f / NS) & 1));
-            double2* sp = slotP + (size_t)s * rowsP * nx;
-            const double2* sr = slotR + (size_t)s * rowsP * nx;
-            const int b0 = row_off * nx, b1 = (row_off + (jhi - jlo)) * nx;
-            for (int idx = b0 + threadIdx.x; idx < b1; idx += blockDim.x) {
-                double2 r = sr[idx];
-                sp[idx] = first ? r : cfma(beta, sp[idx], r);
+            double2* sp = slotP + (size_t)s * rowsP * W;
+            const double2* sr = slotR + (size_t)s * rowsP * W;
+            for (int r = rlo + rl; r < rhi && act; r += RPT) {
+                const int o = r * W + ci + 1;
+                const double2 rv = sr[o];
+                const double2 pv = first ? rv : cfma(beta, sp[o], rv);
+                sp[o] = pv;
+                const int jr = r - 2;                            // owned row index
+                if (jr >= 0 && jr < ty_own) {
+                    const size_t gi = ((size_t)f * ny + j0 + jr) * nx + ci;
+                    Pout[gi] = pv;
+                    if (FULLX) {
+                        double2* X = a.X + (size_t)rhs * N;
+                        X[gi] = cfma(alpha, pv, X[gi]);
+                    }
+                }
+            }
+        }
+        // ---- B2: phase 3, plane t: A r_{k+1}, reductions, write r_{k+1}
+        if (t >= 0 && t < nz) {
+            const double2* rc = rn + (size_t)(t % 3) * rowsR * W;
+            const double2* rd = rn + (size_t)((t + 2) % 3) * rowsR * W;
+            const double2* ru = rn + (size_t)((t + 1) % 3) * rowsR * W;
+            const bool edge = (t == 0 || t == nz - 1);
+            const double th = edge ? 0.5 : 1.0;
+            const double thx = th * cx, thy = th * cy;
+            const double dre = th * dbase + cz * (edge ? 1.0 : 2.0) + (edge ? a.op.robin : 0.0);
+            const double dim = th * shift;
+            const double wd = t > 0 ? cz : 0.0, wu = t < nz - 1 ? cz : 0.0;
+#pragma unroll
+            for (int m = 0; m < MAXR; ++m) {
+                const int jr = rl + m * RPT;
+                if (!act || jr >= ty_own) break;
+                const int o = (jr + 1) * W + ci + 1;
+                const double2 r0 = rc[o];
+                const double2 sx = cadd(rc[o - 1], rc[o + 1]);
+                const double2 sy = cadd(rc[o - W], rc[o + W]);
+                const double2 zd = rd[o], zu = ru[o];
+                const double dr = fma(th, mu3[m], dre);
+                double2 ar;
+                ar.x = dr * r0.x - dim * r0.y - thx * sx.x - thy * sy.x - wd * zd.x - wu * zu.x;
+                ar.y = dr * r0.y + dim * r0.x - thx * sx.y - thy * sy.y - wd * zd.y - wu * zu.y;
+                acc[0] = fma(r0.x, r0.x, fma(-r0.y, r0.y, acc[0]));
+                acc[1] = fma(2.0 * r0.x, r0.y, acc[1]);
+                acc[2] = fma(r0.x, ar.x, fma(-r0.y, ar.y, acc[2]));
+                acc[3] = fma(r0.x, ar.y, fma(r0.y, ar.x, acc[3]));
+                acc[8] = fma(r0.x, r0.x, fma(r0.y, r0.y, acc[8]));
+                Rout[((size_t)t * ny + j0 + jr) * nx + ci] = r0;
             }
         }
         __syncthreads();
-        // (3) plane g = f - 1: q = A p_k, r_{k+1} = r_k - alpha q  (rows -1 .. TY)
-        const int g = f - 1;
+        // ---- C: phase 2, plane g: q = A p_k, r_{k+1} = r_k - alpha q (slot rows 1 .. TY+2)
         if (g >= 0 && g < nz) {
             const int sg = g % NS;
-            const double2* pc = slotP + (size_t)sg * rowsP * nx;
-            const double2* pd = slotP + (size_t)((g + NS - 1) % NS) * rowsP * nx;   // plane g-1
-            const double2* pu = slotP + (size_t)((g + 1) % NS) * rowsP * nx;        // plane g+1
-            const double2* rc = slotR + (size_t)sg * rowsP * nx;
-            double2* rno = rn + (size_t)(g % 3) * rowsR * nx;
-            const double th = theta_of(g, nz);
-            const bool hasD = g > 0, hasU = g < nz - 1;
-            for (int idx = threadIdx.x; idx < rowsR * nx; idx += blockDim.x) {
-                const int lr = idx / nx, i = idx - lr * nx;   // lr = local row + 1
-                const int jg = j0 - 1 + lr;
-                if (jg < 0 || jg >= ny) continue;
-                const int sidx = (lr + 1) * nx + i;           // row in slot coords
-                const double2 p0 = pc[sidx];
-                double2 lat = cmk(0, 0);
-                if (i > 0) lat = cadd(lat, cscale(pc[sidx - 1], cx));
-                if (i < nx - 1) lat = cadd(lat, cscale(pc[sidx + 1], cx));
-                lat = cadd(lat, cscale(cadd(pc[sidx - nx], pc[sidx + nx]), cy));
-                double2 zz = cmk(0, 0);
-                if (hasD) zz = cadd(zz, pd[sidx]);
-                if (hasU) zz = cadd(zz, pu[sidx]);
-                const double mu = a.mu[((size_t)g * ny + jg) * nx + i];
-                const double2 dg = diag_of(a.op, g, mu, shift);
-                double2 q = cmul(dg, p0);
-                q = csub(q, cscale(lat, th));
-                q = csub(q, cscale(zz, cz));
-                const double2 rnew = csub(rc[sidx], cmul(alpha, q));
-                rno[idx] = rnew;
-                if (lr >= 1 && lr <= ty_own) {
-                    // nu += r_{k+1} q ; sigma_direct += p_k q   (bilinear)
+            const double2* pc = slotP + (size_t)sg * rowsP * W;
+            const double2* pd = slotP + (size_t)((g + NS - 1) % NS) * rowsP * W;
+            const double2* pu = slotP + (size_t)((g + 1) % NS) * rowsP * W;
+            const double2* rc = slotR + (size_t)sg * rowsP * W;
+            double2* rno = rn + (size_t)(g % 3) * rowsR * W;
+            const bool edge = (g == 0 || g == nz - 1);
+            const double th = edge ? 0.5 : 1.0;
+            const double thx = th * cx, thy = th * cy;
+            const double dre = th * dbase + cz * (edge ? 1.0 : 2.0) + (edge ? a.op.robin : 0.0);
+            const double dim = th * shift;
+            const double wd = g > 0 ? cz : 0.0, wu = g < nz - 1 ? cz : 0.0;
+            const int r2lo = max(1, rlo), r2hi = min(TY + 3, rhi);
+#pragma unroll
+            for (int m = 0; m < MAXR; ++m) {
+                const int r = 1 + rl + m * RPT;
+                if (!act || r > TY + 2) break;
+                if (r < r2lo || r >= r2hi) continue;
+                const int o = r * W + ci + 1;
+                const double2 p0 = pc[o];
+                const double2 sx = cadd(pc[o - 1], pc[o + 1]);
+                const double2 sy = cadd(pc[o - W], pc[o + W]);
+                const double2 zd = pd[o], zu = pu[o];
+                const double dr = fma(th, mu2[m], dre);
+                double2 q;
+                q.x = dr * p0.x - dim * p0.y - thx * sx.x - thy * sy.x - wd * zd.x - wu * zu.x;
+                q.y = dr * p0.y + dim * p0.x - thx * sx.y - thy * sy.y - wd * zd.y - wu * zu.y;
+                const double2 rnew = csub(rc[o], cmul(alpha, q));
+                rno[o - W] = rnew;
+                const int jr = r - 2;
+                if (jr >= 0 && jr < ty_own) {
                     acc[4] = fma(rnew.x, q.x, fma(-rnew.y, q.y, acc[4]));
                     acc[5] = fma(rnew.x, q.y, fma(rnew.y, q.x, acc[5]));
                     acc[6] = fma(p0.x, q.x, fma(-p0.y, q.y, acc[6]));
                     acc[7] = fma(p0.x, q.y, fma(p0.y, q.x, acc[7]));
                 }
             }
-        }
-        __syncthreads();
-        // (4) plane t = f - 2: A r_{k+1}, reductions, write r_{k+1}, p_k, samples
-        const int t = f - 2;
-        if (t >= 0 && t < nz) {
-            const double2* rc = rn + (size_t)(t % 3) * rowsR * nx;
-            const double2* rd = rn + (size_t)((t + 2) % 3) * rowsR * nx;   // plane t-1
-            const double2* ru = rn + (size_t)((t + 1) % 3) * rowsR * nx;   // plane t+1
-            const double2* pt = slotP + (size_t)(t % NS) * rowsP * nx;
-            const double th = theta_of(t, nz);
-            const bool hasD = t > 0, hasU = t < nz - 1;
-            const size_t gbase = ((size_t)t * ny + j0) * nx;
-            for (int idx = threadIdx.x; idx < ty_own * nx; idx += blockDim.x) {
-                const int lr = idx / nx, i = idx - lr * nx;
-                const int ridx = (lr + 1) * nx + i;
-                const double2 r0 = rc[ridx];
-                double2 lat = cmk(0, 0);
-                if (i > 0) lat = cadd(lat, cscale(rc[ridx - 1], cx));
-                if (i < nx - 1) lat = cadd(lat, cscale(rc[ridx + 1], cx));
-                lat = cadd(lat, cscale(cadd(rc[ridx - nx], rc[ridx + nx]), cy));
-                double2 zz = cmk(0, 0);
-                if (hasD) zz = cadd(zz, rd[ridx]);
-                if (hasU) zz = cadd(zz, ru[ridx]);
-                const double mu = a.mu[gbase + idx];
-                const double2 dg = diag_of(a.op, t, mu, shift);
-                double2 ar = cmul(dg, r0);
-                ar = csub(ar, cscale(lat, th));
-                ar = csub(ar, cscale(zz, cz));
-                acc[0] = fma(r0.x, r0.x, fma(-r0.y, r0.y, acc[0]));
-                acc[1] = fma(2.0 * r0.x, r0.y, acc[1]);
-                acc[2] = fma(r0.x, ar.x, fma(-r0.y, ar.y, acc[2]));
-                acc[3] = fma(r0.x, ar.y, fma(r0.y, ar.x, acc[3]));
-                acc[8] = fma(r0.x, r0.x, fma(r0.y, r0.y, acc[8]));
-                const double2 pk = pt[(lr + 2) * nx + i];
-                Rout[gbase + idx] = r0;
-                Pout[gbase + idx] = pk;
-                if (FULLX) {
-                    double2* X = a.X + (size_t)rhs * N;
-                    X[gbase + idx] = cfma(alpha, pk, X[gbase + idx]);
-                }
-            }
             if (!FULLX && a.nP > 0) {
-                const int s0 = soff[(size_t)t * a.tl.ntiles], s1 = soff[(size_t)t * a.tl.ntiles + 1];
+                const int s0 = soff[(size_t)g * a.tl.ntiles], s1 = soff[(size_t)g * a.tl.ntiles + 1];
                 double2* XP = a.XP + (size_t)rhs * a.nP;
                 for (int sidx = s0 + threadIdx.x; sidx < s1; sidx += blockDim.x) {
-                    const int node = a.samp_nodes[sidx];
-                    const int rem = node - t * nx * ny;
+                    const int rem = a.samp_nodes[sidx] - g * nx * ny;
                     const int jg = rem / nx, i = rem - jg * nx;
-                    const double2 pk = pt[(jg - j0 + 2) * nx + i];
-                    XP[sidx] = cfma(alpha, pk, XP[sidx]);
+                    XP[sidx] = cfma(alpha, pc[(jg - j0 + 2) * W + i + 1], XP[sidx]);
                 }
             }
         }
@@ -314,7 +340,7 @@ __global__ void __launch_bounds__(512, 1) cocg_pass_kernel(const PassArgs a) {
     block_reduce_partials(acc, scratch);
     if (threadIdx.x == 0) {
         double* out = a.part[kout] + ((size_t)rhs * a.tl.ntiles + tile) * kNumPartials;
-        for (int i = 0; i < kNumPartials; ++i) out[i] = acc[i];
+        for (int q = 0; q < kNumPartials; ++q) out[q] = acc[q];
     }
 }
 
@@ -412,30 +438,27 @@ __global__ void fill_shift_kernel(double* shift, int nb, long long rg0, int ncol
 
 }  // namespace
 
-CocgTiling cocg_tiling(int nx, int ny, int nz) {
+CocgTiling cocg_tiling(int nx, int ny, int nz, int prefetch, size_t max_smem) {
     CocgTiling t;
-    const size_t budget = 220 * 1024;
-    const size_t row = (size_t)nx * sizeof(double2);
-    auto smem_of = [&](int TY, int NS) {
+    const size_t budget = max_smem ? max_smem : 225 * 1024;
+    const int NS = prefetch + 3;
+    const int RPT = std::max(1, 512 / nx);
+    const size_t row = (size_t)(nx + 2) * sizeof(double2);
+    auto smem_of = [&](int TY) {
         return (size_t)NS * 2 * (TY + 4) * row + 3 * (TY + 2) * row + NS * 8 + (16 * kNumPartials + 8) * 8 + 256;
     };
-    int best = 0, bestNS = 4;
-    for (int NS = 5; NS >= 4; --NS) {
-        int TY = 0;
-        for (int ty = 1; ty <= ny; ++ty)
-            if (smem_of(ty, NS) <= budget) TY = ty;
-        if (NS == 5 && TY >= 12) { best = TY; bestNS = 5; break; }
-        if (NS == 4) { best = TY; bestNS = 4; }
-    }
+    int best = 0;
+    // phase loops cover at most MAXR = 4 rows per thread: TY + 2 <= 4 RPT
+    for (int ty = 1; ty <= ny && ty + 2 <= 4 * RPT; ++ty)
+        if (smem_of(ty) <= budget) best = ty;
     if (best <= 0) throw Error(DOT_ERR_ARG, "grid rows too long for the shared-memory plane ring (nx too large)");
-    // balance tiles: same count, smaller rows
-    int ntiles = (ny + best - 1) / best;
-    int TY = (ny + ntiles - 1) / ntiles;
-    t.TY = TY;
-    t.ntiles = ntiles;
-    t.nslots = bestNS;
-    t.threads = 512;
-    t.smem = smem_of(TY, bestNS);
+    const int ntiles = (ny + best - 1) / best;
+    t.TY = (ny + ntiles - 1) / ntiles;      // balanced tiles
+    t.ntiles = (ny + t.TY - 1) / t.TY;
+    t.nslots = NS;
+    t.rpt = RPT;
+    t.threads = (nx * RPT + 31) / 32 * 32;
+    t.smem = smem_of(t.TY);
     return t;
 }
 

@@ -11,9 +11,11 @@ namespace dot {
 // copies into a ring of `nslots` shared-memory slots.
 struct CocgTiling {
     int TY = 0, ntiles = 0, nslots = 0, threads = 512;
+    int rpt = 0;          // x-rows covered by one sweep of the block (threads = roundup32(nx * rpt))
     size_t smem = 0;
 };
-CocgTiling cocg_tiling(int nx, int ny, int nz);
+// prefetch: planes loaded ahead (slots = prefetch + 3); max_smem: per-CTA budget (bytes)
+CocgTiling cocg_tiling(int nx, int ny, int nz, int prefetch = 1, size_t max_smem = 0);
 
 struct PassArgs {
     OpConst op;
