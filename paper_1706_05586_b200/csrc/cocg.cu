@@ -9,6 +9,8 @@
 // sigma_k = p_k^T q_k.  The next pass takes beta_{k+1} = rho_{k+1}/rho_k,
 // sigma_{k+1} = mu_{k+1} + 2 beta nu_{k+1} + beta^2 sigma_k, alpha = rho/sigma.
 // HBM traffic per point and iteration: read r, p; write r, p = 64 B.
+#include <vector>
+
 #include "kernels.h"
 
 namespace dot {
@@ -130,29 +132,36 @@ __device__ Scalars pass_scalars(const PassArgs& a, int rhs, int tile) {
 // Shared memory: NS plane slots for r_k and p_{k-1} -> p_k ([TY+4 rows][nx+2] with zero
 // guard columns = Dirichlet x-faces, zero rows outside the y-range), and a ring of 3
 // r_{k+1} planes ([TY+2][nx+2]).  Step f of the z-march:
-//   A  issue bulk copies of plane f+PD                        (warp 0)
+//   A  bulk copies of plane f+PD into smem (warp 0); L2 prefetch of plane f+LPD (warp 1)
 //   B  p_k(f) = r_k(f) + beta p_{k-1}(f); write p_k(f) rows    (phase 1)
 //      A r_{k+1} at plane f-3, reductions, write r_{k+1}(f-3)  (phase 3)
 //   -- barrier --
 //   C  q = A p_k at plane f-1, r_{k+1}(f-1) = r_k - alpha q, reductions, samples
 //   -- barrier --
-template <bool FULLX>
+// Template parameters fix the geometry at compile time (0 = read at run time).
+template <bool FULLX, int NX_, int TY_, int NS_, int RPT_>
 __global__ void __launch_bounds__(512, 1) cocg_pass_kernel(const PassArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int MAXR = 4;                       // rows per thread per phase (tiling guarantees)
+    constexpr int LPD = 4;                        // L2 prefetch distance (planes)
     const int tile = blockIdx.x, rhs = blockIdx.y;
-    const int nx = a.op.nx, ny = a.op.ny, nz = a.op.nz;
-    const int TY = a.tl.TY, NS = a.tl.nslots, RPT = a.tl.rpt;
+    const int nx = NX_ ? NX_ : a.op.nx;
+    const int ny = a.op.ny, nz = a.op.nz;
+    const int TY = TY_ ? TY_ : a.tl.TY;
+    const int NS = NS_ ? NS_ : a.tl.nslots;
+    const int RPT = RPT_ ? RPT_ : a.tl.rpt;
+    const int ntiles = a.tl.ntiles;
     const int W = nx + 2;                          // padded row stride
     const int rowsP = TY + 4, rowsR = TY + 2;
-    const size_t N = (size_t)nx * ny * nz;
+    const int PS = nx * ny;                        // plane stride (elements)
+    const size_t N = (size_t)PS * nz;
     const int j0 = tile * TY;
     const int ty_own = min(TY, ny - j0);
 
     double2* slotR = reinterpret_cast<double2*>(smem_raw);                 // [NS][rowsP][W]
-    double2* slotP = slotR + (size_t)NS * rowsP * W;                        // [NS][rowsP][W]
-    double2* rn = slotP + (size_t)NS * rowsP * W;                           // [3][rowsR][W]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(rn + (size_t)3 * rowsR * W);
+    double2* slotP = slotR + NS * rowsP * W;                                // [NS][rowsP][W]
+    double2* rn = slotP + NS * rowsP * W;                                   // [3][rowsR][W]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(rn + 3 * rowsR * W);
     double* scratch = reinterpret_cast<double*>(bars + NS);
     __shared__ Scalars sh_sc;
 
@@ -168,12 +177,15 @@ __global__ void __launch_bounds__(512, 1) cocg_pass_kernel(const PassArgs a) {
     const double2* __restrict__ Pin = a.Pv[kin] + (size_t)rhs * N;
     double2* __restrict__ Rout = a.R[kout] + (size_t)rhs * N;
     double2* __restrict__ Pout = a.Pv[kout] + (size_t)rhs * N;
+    double2* __restrict__ Xf = FULLX ? a.X + (size_t)rhs * N : nullptr;
     const double* __restrict__ mu = a.mu;
+    const double cx = a.op.cx, cy = a.op.cy, cz = a.op.cz, robin = a.op.robin;
 
     // slot rows holding in-domain grid rows: [rlo, rhi); grid row of slot row r = j0 - 2 + r
     const int rlo = max(0, 2 - j0), rhi = min(rowsP, ny - j0 + 2);
     const uint32_t row_bytes = (uint32_t)(nx * sizeof(double2));
     const uint32_t plane_bytes = (uint32_t)(rhi - rlo) * row_bytes;
+    const int tile_off = (j0 - 2 + rlo) * nx;      // first in-domain element of a plane tile
 
     for (int idx = threadIdx.x; idx < NS * rowsP * W; idx += blockDim.x) {
         slotR[idx] = cmk(0, 0);
@@ -188,30 +200,59 @@ __global__ void __launch_bounds__(512, 1) cocg_pass_kernel(const PassArgs a) {
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int PD = NS - 3;
-    // warp 0: lane 0 arms the barrier, then the lanes issue one bulk copy per row
-    auto issue = [&](int z) {
+    auto issue = [&](int z) {       // warp 0: lane 0 arms the barrier, lanes copy one row each
         const int s = z % NS;
         if (lane == 0) {
             fence_proxy_async();
             mbar_expect_tx(&bars[s], first ? plane_bytes : 2 * plane_bytes);
         }
         __syncwarp();
+        const int gz = z * PS + (j0 - 2) * nx;
         for (int r = rlo + lane; r < rhi; r += 32) {
-            const size_t g = ((size_t)z * ny + (j0 - 2 + r)) * nx;
-            const size_t o = ((size_t)s * rowsP + r) * W + 1;
-            bulk_g2s(slotR + o, Rin + g, row_bytes, &bars[s]);
-            if (!first) bulk_g2s(slotP + o, Pin + g, row_bytes, &bars[s]);
+            const int o = (s * rowsP + r) * W + 1;
+            bulk_g2s(slotR + o, Rin + gz + r * nx, row_bytes, &bars[s]);
+            if (!first) bulk_g2s(slotP + o, Pin + gz + r * nx, row_bytes, &bars[s]);
         }
+    };
+    auto prefetch_l2 = [&](int z) {   // one contiguous block per vector
+        const int gz = z * PS + tile_off;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Rin + gz), "r"(plane_bytes) : "memory");
+        if (!first)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Pin + gz), "r"(plane_bytes) : "memory");
     };
     if (warp == 0)
         for (int z = 0; z < PD && z < nz; ++z) issue(z);
+    if (warp == 1 && lane == 0)
+        for (int z = PD; z < PD + LPD && z < nz; ++z) prefetch_l2(z);
 
+    // ---- per-thread geometry, fixed for the whole march
     const bool act = threadIdx.x < nx * RPT;
-    const int ci = act ? threadIdx.x % nx : 0;       // my column
-    const int rl = act ? threadIdx.x / nx : RPT;     // my first row within a sweep
-    const double cx = a.op.cx, cy = a.op.cy, cz = a.op.cz;
+    const int ci = act ? threadIdx.x % nx : 0;
+    const int rl = act ? threadIdx.x / nx : RPT;
+    int p1s[MAXR], p1g[MAXR];        // phase 1: slot offset, global offset in plane (-1: not owned)
+    bool p1v[MAXR];
+    int p3s[MAXR], p3g[MAXR];        // phase 3 (owned rows): rn offset, global offset
+    bool p3v[MAXR];
+    int p2s[MAXR], p2g[MAXR];        // phase C: slot offset, mu offset in plane
+    bool p2v[MAXR], p2o[MAXR];
+#pragma unroll
+    for (int m = 0; m < MAXR; ++m) {
+        const int r1 = rlo + rl + m * RPT;
+        p1v[m] = act && r1 < rhi;
+        p1s[m] = r1 * W + ci + 1;
+        p1g[m] = (r1 - 2 >= 0 && r1 - 2 < ty_own) ? (j0 + r1 - 2) * nx + ci : -1;
+        const int jr = rl + m * RPT;
+        p3v[m] = act && jr < ty_own;
+        p3s[m] = (jr + 1) * W + ci + 1;
+        p3g[m] = (j0 + jr) * nx + ci;
+        const int r2 = 1 + rl + m * RPT;
+        p2v[m] = act && r2 <= TY + 2 && r2 >= rlo && r2 < rhi;
+        p2s[m] = r2 * W + ci + 1;
+        p2g[m] = (j0 - 2 + r2) * nx + ci;
+        p2o[m] = (r2 - 2 >= 0 && r2 - 2 < ty_own);
+    }
     const double dbase = 2.0 * cx + 2.0 * cy;
-    const int32_t* soff = a.samp_off + (size_t)tile;
+    const int32_t* soff = a.samp_off + tile;
 
     double acc[kNumPartials];
 #pragma unroll
@@ -219,56 +260,50 @@ __global__ void __launch_bounds__(512, 1) cocg_pass_kernel(const PassArgs a) {
 
     for (int f = 0; f < nz + 3; ++f) {
         if (warp == 0 && f + PD < nz) issue(f + PD);
+        if (warp == 1 && lane == 0 && f + PD + LPD < nz) prefetch_l2(f + PD + LPD);
         const int g = f - 1, t = f - 3;
-        // ---- prefetch mu for phase 3 (plane t, owned rows) and phase C (plane g, rows 1..TY+2)
+        const bool do3 = t >= 0 && t < nz, do2 = g >= 0 && g < nz;
         double mu3[MAXR], mu2[MAXR];
 #pragma unroll
         for (int m = 0; m < MAXR; ++m) {
-            const int r3 = rl + m * RPT;                         // owned row offset
-            mu3[m] = (t >= 0 && t < nz && r3 < ty_own) ? mu[((size_t)t * ny + j0 + r3) * nx + ci] : 0.0;
-            const int r2 = 1 + rl + m * RPT;                     // slot row
-            const int jg = j0 - 2 + r2;
-            mu2[m] = (g >= 0 && g < nz && r2 <= TY + 2 && jg >= 0 && jg < ny)
-                         ? mu[((size_t)g * ny + jg) * nx + ci] : 0.0;
+            mu3[m] = (do3 && p3v[m]) ? mu[t * PS + p3g[m]] : 0.0;
+            mu2[m] = (do2 && p2v[m]) ? mu[g * PS + p2g[m]] : 0.0;
         }
         // ---- B1: phase 1, plane f
         if (f < nz) {
             const int s = f % NS;
             mbar_wait(&bars[s], (uint32_t)((f / NS) & 1));
-            double2* sp = slotP + (size_t)s * rowsP * W;
-            const double2* sr = slotR + (size_t)s * rowsP * W;
-            for (int r = rlo + rl; r < rhi && act; r += RPT) {
-                const int o = r * W + ci + 1;
-                const double2 rv = sr[o];
-                const double2 pv = first ? rv : cfma(beta, sp[o], rv);
-                sp[o] = pv;
-                const int jr = r - 2;                            // owned row index
-                if (jr >= 0 && jr < ty_own) {
-                    const size_t gi = ((size_t)f * ny + j0 + jr) * nx + ci;
-                    Pout[gi] = pv;
-                    if (FULLX) {
-                        double2* X = a.X + (size_t)rhs * N;
-                        X[gi] = cfma(alpha, pv, X[gi]);
-                    }
+            double2* sp = slotP + s * rowsP * W;
+            const double2* sr = slotR + s * rowsP * W;
+            const int fo = f * PS;
+#pragma unroll
+            for (int m = 0; m < MAXR; ++m) {
+                if (!p1v[m]) continue;
+                const double2 rv = sr[p1s[m]];
+                const double2 pv = first ? rv : cfma(beta, sp[p1s[m]], rv);
+                sp[p1s[m]] = pv;
+                if (p1g[m] >= 0) {
+                    Pout[fo + p1g[m]] = pv;
+                    if (FULLX) Xf[fo + p1g[m]] = cfma(alpha, pv, Xf[fo + p1g[m]]);
                 }
             }
         }
         // ---- B2: phase 3, plane t: A r_{k+1}, reductions, write r_{k+1}
-        if (t >= 0 && t < nz) {
-            const double2* rc = rn + (size_t)(t % 3) * rowsR * W;
-            const double2* rd = rn + (size_t)((t + 2) % 3) * rowsR * W;
-            const double2* ru = rn + (size_t)((t + 1) % 3) * rowsR * W;
+        if (do3) {
+            const double2* rc = rn + (t % 3) * rowsR * W;
+            const double2* rd = rn + ((t + 2) % 3) * rowsR * W;
+            const double2* ru = rn + ((t + 1) % 3) * rowsR * W;
             const bool edge = (t == 0 || t == nz - 1);
             const double th = edge ? 0.5 : 1.0;
             const double thx = th * cx, thy = th * cy;
-            const double dre = th * dbase + cz * (edge ? 1.0 : 2.0) + (edge ? a.op.robin : 0.0);
+            const double dre = th * dbase + cz * (edge ? 1.0 : 2.0) + (edge ? robin : 0.0);
             const double dim = th * shift;
             const double wd = t > 0 ? cz : 0.0, wu = t < nz - 1 ? cz : 0.0;
+            const int to = t * PS;
 #pragma unroll
             for (int m = 0; m < MAXR; ++m) {
-                const int jr = rl + m * RPT;
-                if (!act || jr >= ty_own) break;
-                const int o = (jr + 1) * W + ci + 1;
+                if (!p3v[m]) continue;
+                const int o = p3s[m];
                 const double2 r0 = rc[o];
                 const double2 sx = cadd(rc[o - 1], rc[o + 1]);
                 const double2 sy = cadd(rc[o - W], rc[o + W]);
@@ -282,31 +317,28 @@ __global__ void __launch_bounds__(512, 1) cocg_pass_kernel(const PassArgs a) {
                 acc[2] = fma(r0.x, ar.x, fma(-r0.y, ar.y, acc[2]));
                 acc[3] = fma(r0.x, ar.y, fma(r0.y, ar.x, acc[3]));
                 acc[8] = fma(r0.x, r0.x, fma(r0.y, r0.y, acc[8]));
-                Rout[((size_t)t * ny + j0 + jr) * nx + ci] = r0;
+                Rout[to + p3g[m]] = r0;
             }
         }
         __syncthreads();
         // ---- C: phase 2, plane g: q = A p_k, r_{k+1} = r_k - alpha q (slot rows 1 .. TY+2)
-        if (g >= 0 && g < nz) {
+        if (do2) {
             const int sg = g % NS;
-            const double2* pc = slotP + (size_t)sg * rowsP * W;
-            const double2* pd = slotP + (size_t)((g + NS - 1) % NS) * rowsP * W;
-            const double2* pu = slotP + (size_t)((g + 1) % NS) * rowsP * W;
-            const double2* rc = slotR + (size_t)sg * rowsP * W;
-            double2* rno = rn + (size_t)(g % 3) * rowsR * W;
+            const double2* pc = slotP + sg * rowsP * W;
+            const double2* pd = slotP + ((g + NS - 1) % NS) * rowsP * W;
+            const double2* pu = slotP + ((g + 1) % NS) * rowsP * W;
+            const double2* rc = slotR + sg * rowsP * W;
+            double2* rno = rn + (g % 3) * rowsR * W - W;          // slot row r -> rn row r - 1
             const bool edge = (g == 0 || g == nz - 1);
             const double th = edge ? 0.5 : 1.0;
             const double thx = th * cx, thy = th * cy;
-            const double dre = th * dbase + cz * (edge ? 1.0 : 2.0) + (edge ? a.op.robin : 0.0);
+            const double dre = th * dbase + cz * (edge ? 1.0 : 2.0) + (edge ? robin : 0.0);
             const double dim = th * shift;
             const double wd = g > 0 ? cz : 0.0, wu = g < nz - 1 ? cz : 0.0;
-            const int r2lo = max(1, rlo), r2hi = min(TY + 3, rhi);
 #pragma unroll
             for (int m = 0; m < MAXR; ++m) {
-                const int r = 1 + rl + m * RPT;
-                if (!act || r > TY + 2) break;
-                if (r < r2lo || r >= r2hi) continue;
-                const int o = r * W + ci + 1;
+                if (!p2v[m]) continue;
+                const int o = p2s[m];
                 const double2 p0 = pc[o];
                 const double2 sx = cadd(pc[o - 1], pc[o + 1]);
                 const double2 sy = cadd(pc[o - W], pc[o + W]);
@@ -316,9 +348,8 @@ __global__ void __launch_bounds__(512, 1) cocg_pass_kernel(const PassArgs a) {
                 q.x = dr * p0.x - dim * p0.y - thx * sx.x - thy * sy.x - wd * zd.x - wu * zu.x;
                 q.y = dr * p0.y + dim * p0.x - thx * sx.y - thy * sy.y - wd * zd.y - wu * zu.y;
                 const double2 rnew = csub(rc[o], cmul(alpha, q));
-                rno[o - W] = rnew;
-                const int jr = r - 2;
-                if (jr >= 0 && jr < ty_own) {
+                rno[o] = rnew;
+                if (p2o[m]) {
                     acc[4] = fma(rnew.x, q.x, fma(-rnew.y, q.y, acc[4]));
                     acc[5] = fma(rnew.x, q.y, fma(rnew.y, q.x, acc[5]));
                     acc[6] = fma(p0.x, q.x, fma(-p0.y, q.y, acc[6]));
@@ -326,10 +357,10 @@ __global__ void __launch_bounds__(512, 1) cocg_pass_kernel(const PassArgs a) {
                 }
             }
             if (!FULLX && a.nP > 0) {
-                const int s0 = soff[(size_t)g * a.tl.ntiles], s1 = soff[(size_t)g * a.tl.ntiles + 1];
+                const int s0 = soff[g * ntiles], s1 = soff[g * ntiles + 1];
                 double2* XP = a.XP + (size_t)rhs * a.nP;
                 for (int sidx = s0 + threadIdx.x; sidx < s1; sidx += blockDim.x) {
-                    const int rem = a.samp_nodes[sidx] - g * nx * ny;
+                    const int rem = a.samp_nodes[sidx] - g * PS;
                     const int jg = rem / nx, i = rem - jg * nx;
                     XP[sidx] = cfma(alpha, pc[(jg - j0 + 2) * W + i + 1], XP[sidx]);
                 }
@@ -339,7 +370,7 @@ __global__ void __launch_bounds__(512, 1) cocg_pass_kernel(const PassArgs a) {
     }
     block_reduce_partials(acc, scratch);
     if (threadIdx.x == 0) {
-        double* out = a.part[kout] + ((size_t)rhs * a.tl.ntiles + tile) * kNumPartials;
+        double* out = a.part[kout] + ((size_t)rhs * ntiles + tile) * kNumPartials;
         for (int q = 0; q < kNumPartials; ++q) out[q] = acc[q];
     }
 }
@@ -468,24 +499,40 @@ void launch_cocg_init(const PassArgs& a, int nb, cudaStream_t s) {
     DOT_CUDA_TRY(cudaGetLastError());
 }
 
-void launch_cocg_pass(const PassArgs& a, int nb, cudaStream_t s) {
-    dim3 grid(a.tl.ntiles, nb);
-    static size_t attr_set[2] = {0, 0};
-    const int which = a.X ? 1 : 0;
-    if (attr_set[which] < a.tl.smem) {
-        if (which)
-            DOT_CUDA_TRY(cudaFuncSetAttribute(cocg_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)a.tl.smem));
-        else
-            DOT_CUDA_TRY(cudaFuncSetAttribute(cocg_pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)a.tl.smem));
-        attr_set[which] = a.tl.smem;
+// Compile-time geometries of the BASELINE.json grids (nx, TY, slots, rows per sweep);
+// any other geometry runs the run-time-parameter instance <.., 0, 0, 0, 0>.
+#define DOT_COCG_GEOMS(X) X(16, 16, 4, 32) X(32, 32, 4, 16) X(64, 16, 4, 8) X(96, 9, 4, 5) X(128, 6, 4, 4)
+
+template <bool FX>
+static void launch_pass_impl(const PassArgs& a, int nb, cudaStream_t s) {
+    using K = void (*)(const PassArgs);
+    K k = cocg_pass_kernel<FX, 0, 0, 0, 0>;
+#define DOT_PICK(GX, GT, GS, GR) \
+    if (a.op.nx == GX && a.tl.TY == GT && a.tl.nslots == GS && a.tl.rpt == GR) k = cocg_pass_kernel<FX, GX, GT, GS, GR>;
+    DOT_COCG_GEOMS(DOT_PICK)
+#undef DOT_PICK
+    static std::vector<std::pair<K, size_t>> attr;
+    bool found = false;
+    for (auto& e : attr)
+        if (e.first == k) {
+            found = true;
+            if (e.second < a.tl.smem) {
+                DOT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.tl.smem));
+                e.second = a.tl.smem;
+            }
+        }
+    if (!found) {
+        DOT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.tl.smem));
+        attr.emplace_back(k, a.tl.smem);
     }
-    if (which)
-        cocg_pass_kernel<true><<<grid, a.tl.threads, a.tl.smem, s>>>(a);
-    else
-        cocg_pass_kernel<false><<<grid, a.tl.threads, a.tl.smem, s>>>(a);
+    dim3 grid(a.tl.ntiles, nb);
+    k<<<grid, a.tl.threads, a.tl.smem, s>>>(a);
     DOT_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_cocg_pass(const PassArgs& a, int nb, cudaStream_t s) {
+    if (a.X) launch_pass_impl<true>(a, nb, s);
+    else launch_pass_impl<false>(a, nb, s);
 }
 
 void launch_count_active(const RhsState* st, int nb, int* d_count, cudaStream_t s) {

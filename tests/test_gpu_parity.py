@@ -18,6 +18,9 @@ GRIDS = [
     dict(n=(16, 16, 16), L=(4.0, 4.0, 4.0)),
     dict(n=(64, 37, 6), L=(8.0, 5.0, 2.0), src=(4, 2), det=(3, 3)),
     dict(n=(33, 21, 9), L=(4.0, 3.0, 2.0), src=(3, 2), det=(2, 3)),
+    # geometries of the compile-time specialised pass kernels (nx=64/TY=16, nx=32/TY=32)
+    dict(n=(64, 64, 5), L=(8.0, 8.0, 1.0), src=(4, 4), det=(4, 4)),
+    dict(n=(32, 32, 6), L=(4.0, 4.0, 1.5), src=(4, 2), det=(2, 4)),
 ]
 
 
