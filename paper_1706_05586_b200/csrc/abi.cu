@@ -425,7 +425,8 @@ int dot_create(const dot_config* cfg, dot_problem** out) {
             const char* eSM = std::getenv("DOT_COCG_SMEM_KB");
             const int pd = ePD ? std::max(1, std::atoi(ePD)) : 1;
             const size_t sm = eSM ? (size_t)std::atoi(eSM) * 1024 : 0;
-            P->tl = cocg_tiling(P->nx, P->ny, P->nz, pd, sm);
+            const char* eTH = std::getenv("DOT_COCG_THREADS");
+            P->tl = cocg_tiling(P->nx, P->ny, P->nz, pd, sm, eTH ? std::atoi(eTH) : 0);
         }
         P->pc = PalsConst{P->nx, P->ny, P->nz, P->n_rbf, P->hx, P->hy, P->hz, P->gamma, P->eps, P->cutoff,
                           P->mua_in, P->mua_out};

@@ -237,7 +237,8 @@ __global__ void __launch_bounds__(512, 1) cocg_pass_kernel(const PassArgs a) {
     bool p2v[MAXR], p2o[MAXR];
 #pragma unroll
     for (int m = 0; m < MAXR; ++m) {
-        const int r1 = rlo + rl + m * RPT;
+        // phase 1 covers TY+4 rows: give its extra rows to the threads with fewer phase-C rows
+        const int r1 = rlo + (act ? (rl + RPT / 2) % RPT : RPT) + m * RPT;
         p1v[m] = act && r1 < rhi;
         p1s[m] = r1 * W + ci + 1;
         p1g[m] = (r1 - 2 >= 0 && r1 - 2 < ty_own) ? (j0 + r1 - 2) * nx + ci : -1;
@@ -469,18 +470,18 @@ __global__ void fill_shift_kernel(double* shift, int nb, long long rg0, int ncol
 
 }  // namespace
 
-CocgTiling cocg_tiling(int nx, int ny, int nz, int prefetch, size_t max_smem) {
+CocgTiling cocg_tiling(int nx, int ny, int nz, int prefetch, size_t max_smem, int max_threads) {
     CocgTiling t;
     const size_t budget = max_smem ? max_smem : 225 * 1024;
     const int NS = prefetch + 3;
-    const int RPT = std::max(1, 512 / nx);
+    const int RPT = std::max(1, (max_threads > 0 ? std::min(max_threads, 512) : 512) / nx);
     const size_t row = (size_t)(nx + 2) * sizeof(double2);
     auto smem_of = [&](int TY) {
         return (size_t)NS * 2 * (TY + 4) * row + 3 * (TY + 2) * row + NS * 8 + (16 * kNumPartials + 8) * 8 + 256;
     };
     int best = 0;
-    // phase loops cover at most MAXR = 4 rows per thread: TY + 2 <= 4 RPT
-    for (int ty = 1; ty <= ny && ty + 2 <= 4 * RPT; ++ty)
+    // phase loops cover at most MAXR = 4 rows per thread; phase 1 has TY + 4 rows
+    for (int ty = 1; ty <= ny && ty + 4 <= 4 * RPT; ++ty)
         if (smem_of(ty) <= budget) best = ty;
     if (best <= 0) throw Error(DOT_ERR_ARG, "grid rows too long for the shared-memory plane ring (nx too large)");
     const int ntiles = (ny + best - 1) / best;

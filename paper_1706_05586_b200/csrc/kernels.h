@@ -15,7 +15,7 @@ struct CocgTiling {
     size_t smem = 0;
 };
 // prefetch: planes loaded ahead (slots = prefetch + 3); max_smem: per-CTA budget (bytes)
-CocgTiling cocg_tiling(int nx, int ny, int nz, int prefetch = 1, size_t max_smem = 0);
+CocgTiling cocg_tiling(int nx, int ny, int nz, int prefetch = 1, size_t max_smem = 0, int max_threads = 0);
 
 struct PassArgs {
     OpConst op;

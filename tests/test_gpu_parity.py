@@ -235,3 +235,27 @@ def test_optimize_directions_parity(dot):
             Qb, _ = np.linalg.qr(B)
             assert np.abs(Qa @ Qa.T - Qb @ Qb.T).max() < 1e-6
         assert np.allclose(np.linalg.norm(Wg[:, -1]), 3.0)
+
+
+@pytest.mark.parametrize("knobs", [dict(DOT_COCG_THREADS="256"), dict(DOT_COCG_THREADS="128"),
+                                   dict(DOT_COCG_SMEM_KB="64"), dict(DOT_COCG_PREFETCH="2"),
+                                   dict(DOT_COCG_THREADS="256", DOT_COCG_SMEM_KB="110")])
+def test_tiling_knobs_keep_parity(dot, knobs, monkeypatch):
+    """Every tiling the run-time knobs can select solves the same systems
+    (guards the generic kernel instance and the tiling constraints)."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    cfg = small_config(**GRIDS[4])
+    prob, wl = small_problem(cfg, with_data=False)
+    g = gpu_problem(dot, cfg, prob, wl)
+    N = prob.grid.N
+    rng = np.random.default_rng(3)
+    b = rng.standard_normal((2, N)) + 1j * rng.standard_normal((2, N))
+    mu = absorption(wl.p, prob.grid, cfg)
+    x, _ = g.solve(b, 1)
+    ref = spla.splu(prob.operator(mu, 1).tocsc()).solve(b.T).T
+    assert rel(x, ref) < 1e-11
+    X = g.solve_sampled(0)
+    samp = g.samples()
+    M = np.transpose(X[:, :, np.searchsorted(samp, wl.det_nodes)], (0, 2, 1))
+    assert rel(M, measurements(prob, wl.p)) < 1e-8
