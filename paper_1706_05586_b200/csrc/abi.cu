@@ -419,14 +419,24 @@ int dot_create(const dot_config* cfg, dot_problem** out) {
         P->op.cy = P->D / (P->hy * P->hy);
         P->op.cz = P->D / (P->hz * P->hz);
         P->op.robin = 1.0 / (2.0 * P->hz);
+        P->op.dint = 2.0 * P->op.cx + 2.0 * P->op.cy + 2.0 * P->op.cz;
         {
             // tuning knobs: planes prefetched, smem budget per CTA
             const char* ePD = std::getenv("DOT_COCG_PREFETCH");
             const char* eSM = std::getenv("DOT_COCG_SMEM_KB");
-            const int pd = ePD ? std::max(1, std::atoi(ePD)) : 1;
-            const size_t sm = eSM ? (size_t)std::atoi(eSM) * 1024 : 0;
             const char* eTH = std::getenv("DOT_COCG_THREADS");
-            P->tl = cocg_tiling(P->nx, P->ny, P->nz, pd, sm, eTH ? std::atoi(eTH) : 0);
+            const char* eK = std::getenv("DOT_COCG_KERNEL");      // "ring" selects the padded-ring pass
+            const char* eTY = std::getenv("DOT_COCG_TY");         // z-pass tile height
+            const int kind = (eK && std::string(eK) == "ring") ? 0 : 1;
+            const int pd = ePD ? std::max(1, std::atoi(ePD)) : (kind == 1 ? 2 : 1);
+            const size_t sm = eSM ? (size_t)std::atoi(eSM) * 1024 : 0;
+            P->tl = cocg_tiling(P->nx, P->ny, P->nz, pd, sm, eTH ? std::atoi(eTH) : 0, kind,
+                                eTY ? std::atoi(eTY) : 0);
+            // cluster of consecutive tiles of one RHS: the largest size <= request dividing ntiles
+            const char* eCL = std::getenv("DOT_COCG_CLUSTER");
+            int cs = eCL ? std::max(1, std::min(8, std::atoi(eCL))) : 1;
+            while (cs > 1 && P->tl.ntiles % cs != 0) --cs;
+            P->tl.cluster = cs;
         }
         P->pc = PalsConst{P->nx, P->ny, P->nz, P->n_rbf, P->hx, P->hy, P->hz, P->gamma, P->eps, P->cutoff,
                           P->mua_in, P->mua_out};

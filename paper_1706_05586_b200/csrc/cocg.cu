@@ -9,6 +9,7 @@
 // sigma_k = p_k^T q_k.  The next pass takes beta_{k+1} = rho_{k+1}/rho_k,
 // sigma_{k+1} = mu_{k+1} + 2 beta nu_{k+1} + beta^2 sigma_k, alpha = rho/sigma.
 // HBM traffic per point and iteration: read r, p; write r, p = 64 B.
+#include <cstdlib>
 #include <vector>
 
 #include "kernels.h"
@@ -470,8 +471,9 @@ __global__ void fill_shift_kernel(double* shift, int nb, long long rg0, int ncol
 
 }  // namespace
 
-CocgTiling cocg_tiling(int nx, int ny, int nz, int prefetch, size_t max_smem, int max_threads) {
+static CocgTiling ring_tiling(int nx, int ny, int nz, int prefetch, size_t max_smem, int max_threads) {
     CocgTiling t;
+    t.kind = 0;
     const size_t budget = max_smem ? max_smem : 225 * 1024;
     const int NS = prefetch + 3;
     const int RPT = std::max(1, (max_threads > 0 ? std::min(max_threads, 512) : 512) / nx);
@@ -492,6 +494,61 @@ CocgTiling cocg_tiling(int nx, int ny, int nz, int prefetch, size_t max_smem, in
     t.threads = (nx * RPT + 31) / 32 * 32;
     t.smem = smem_of(t.TY);
     return t;
+}
+
+// z-register pass tiling (cocg_z.cu): one thread per (x, slot row) of TY + 4 rows.
+// Options in order of preference (measured on B200 at 64^3):
+//   B: <= 768 threads, one CTA per SM (78 registers, no spills)
+//   C: <= 1024 threads (64 registers)      A: <= 512 threads, two CTAs per SM (64 registers)
+// The first option whose tile height reaches 4 rows wins, else the one with the largest TY.
+// DOT_COCG_ZOPT=A|B|C forces one option.
+static bool z_tiling(int nx, int ny, int prefetch, int want_ty, CocgTiling& out) {
+    const int NS = prefetch + 2;
+    const size_t sm_cta = 227 * 1024, sm_sm = 228 * 1024 - 2048;
+    struct Opt { char name; int maxt, minb; };
+    const Opt opts[3] = {{'B', 768, 1}, {'C', 1024, 1}, {'A', 512, 2}};
+    const char* eO = std::getenv("DOT_COCG_ZOPT");
+    CocgTiling best;
+    bool found = false;
+    for (const Opt& o : opts) {
+        if (eO && eO[0] != o.name) continue;
+        int ty = 0;
+        for (int c = 1; c <= ny; ++c) {
+            const int thr = ((c + 4) * nx + 31) / 32 * 32;
+            const size_t sm = zpass_smem(nx, c, NS);
+            if (thr > o.maxt || sm > sm_cta || (size_t)o.minb * (sm + 1024) > sm_sm) break;
+            ty = c;
+            if (want_ty > 0 && c == want_ty) break;
+        }
+        if (want_ty > 0 && ty != want_ty) continue;
+        if (ty <= 0) continue;
+        const int ntiles = (ny + ty - 1) / ty;
+        CocgTiling t;
+        t.kind = 1;
+        t.minb = o.minb;
+        t.TY = (ny + ntiles - 1) / ntiles;
+        t.ntiles = (ny + t.TY - 1) / t.TY;
+        t.nslots = NS;
+        t.threads = ((t.TY + 4) * nx + 31) / 32 * 32;
+        t.smem = zpass_smem(nx, t.TY, NS);
+        if (!found || (best.TY < 4 && t.TY > best.TY)) {
+            best = t;
+            found = true;
+        }
+        if (best.TY >= 4 || want_ty > 0) break;
+    }
+    if (found) out = best;
+    return found;
+}
+
+CocgTiling cocg_tiling(int nx, int ny, int nz, int prefetch, size_t max_smem, int max_threads, int kind,
+                       int want_ty) {
+    if (kind != 0) {
+        CocgTiling t;
+        if (z_tiling(nx, ny, std::max(1, prefetch), want_ty, t)) return t;
+        if (kind == 1 && want_ty > 0) throw Error(DOT_ERR_ARG, "requested z-pass tile height does not fit");
+    }
+    return ring_tiling(nx, ny, nz, std::max(1, prefetch - (kind != 0 ? 1 : 0)), max_smem, max_threads);
 }
 
 void launch_cocg_init(const PassArgs& a, int nb, cudaStream_t s) {
@@ -527,11 +584,14 @@ static void launch_pass_impl(const PassArgs& a, int nb, cudaStream_t s) {
         attr.emplace_back(k, a.tl.smem);
     }
     dim3 grid(a.tl.ntiles, nb);
-    k<<<grid, a.tl.threads, a.tl.smem, s>>>(a);
-    DOT_CUDA_TRY(cudaGetLastError());
+    launch_clustered(k, grid, a.tl.threads, a.tl.smem, s, a.tl.cluster, a);
 }
 
 void launch_cocg_pass(const PassArgs& a, int nb, cudaStream_t s) {
+    if (a.tl.kind == 1) {
+        launch_cocg_zpass(a, nb, s);
+        return;
+    }
     if (a.X) launch_pass_impl<true>(a, nb, s);
     else launch_pass_impl<false>(a, nb, s);
 }

@@ -1,0 +1,439 @@
+// Fused single-pass COCG iteration, z-march with register-resident z-neighbours
+// ("COCG pass tiling"; PAPER.md L966 solves of Eq. (2.1)).
+//
+// Same recurrences as cocg_pass_kernel (cocg.cu): pass k forms
+//   p_k = r_k + beta_k p_{k-1},  q = A p_k,  r_{k+1} = r_k - alpha_k q
+// with rho, mu = r^T A r, nu = r^T q and sigma_direct = p^T q reduced in the same
+// sweep; 64 B of HBM traffic per point and iteration (read r_k, p_{k-1}; write
+// p_k, r_{k+1}).
+//
+// Mapping: a CTA owns TY full x-rows (grid rows j0 .. j0+TY-1) of one RHS and
+// marches the nz planes.  One thread per (x, slot row) of the TY+4 slot rows:
+//   slot rows 2 .. TY+1   own rows:  phase 1 (p_k), 2 (q, r_{k+1}), 3 (A r_{k+1})
+//   slot rows 1, TY+2     y-halo 1:  phases 1, 2   (r_{k+1} feeds the own rows' stencil)
+//   slot rows 0, TY+3     y-halo 2:  phase 1       (p_k feeds the halo-1 stencil)
+// Each thread keeps its own column's p_k and r_{k+1} of the two previous planes
+// in registers, so the z-neighbours of both stencils never touch shared memory;
+// only the 4 in-plane neighbours are read from shared memory.
+//
+// Per plane f (one __syncthreads per plane):
+//   producer  one cp.async.bulk per vector: the TY+4 contiguous rows of r_k and
+//             p_{k-1} of plane f+PD into ring slot (f+PD) % NS   (NS = PD + 2)
+//   phase 1   plane f:   p_k = r_k + beta p_{k-1}, written in place into the slot
+//   phase 2   plane f-1: q = A p_k, r_{k+1} = r_k - alpha q -> Rbuf[(f-1) % 3]
+//   phase 3   plane f-2: A r_{k+1}, reductions, store r_{k+1}
+#include "kernels.h"
+
+namespace dot {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32z(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ double warp_sum_z(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+struct ZScalars {
+    double2 alpha, beta;
+    int active;
+};
+
+// Scalar recurrences of pass k for one RHS, computed by warp 0 (lanes split the
+// tiles, fixed-order butterfly reduction: identical in every CTA of the RHS).
+__device__ void zpass_scalars(const PassArgs& a, int rhs, int tile, ZScalars* out) {
+    const int lane = threadIdx.x & 31;
+    const int ntiles = a.tl.ntiles;
+    const double* pp = a.part[a.k & 1] + (size_t)rhs * ntiles * kNumPartials;
+    double s[kNumPartials];
+#pragma unroll
+    for (int i = 0; i < kNumPartials; ++i) s[i] = 0.0;
+    for (int t = lane; t < ntiles; t += 32)
+#pragma unroll
+        for (int i = 0; i < kNumPartials; ++i) s[i] += pp[t * kNumPartials + i];
+#pragma unroll
+    for (int i = 0; i < kNumPartials; ++i) s[i] = warp_sum_z(s[i]);
+    if (lane != 0) return;
+    const RhsState prev = a.st[(a.k + 1) & 1][rhs];
+    RhsState cur = prev;
+    ZScalars sc;
+    sc.alpha = cmk(0, 0);
+    sc.beta = cmk(0, 0);
+    sc.active = 0;
+    if (!prev.done) {
+        const double2 rho = cmk(s[0], s[1]), mu = cmk(s[2], s[3]), nu = cmk(s[4], s[5]);
+        const double2 sigd = cmk(s[6], s[7]);
+        const double nrm2 = s[8];
+        if (a.k == 0) cur.bnorm2 = nrm2;
+        double2 beta = cmk(0, 0), sigma = mu;
+        if (a.k > 0) {
+            beta = cdiv(rho, cmk(prev.rho_re, prev.rho_im));
+            sigma = cadd(cadd(mu, cscale(cmul(beta, nu), 2.0)), cmul(cmul(beta, beta), sigd));
+        }
+        const double2 alpha = cdiv(rho, sigma);
+        if (!(nrm2 > a.tol2 * cur.bnorm2)) {            // converged (also b = 0)
+            cur.done = 1;
+            cur.iters = a.k;
+        } else if (a.k >= a.max_iter) {
+            cur.done = 1;
+            cur.iters = a.k;
+            cur.flag = DOT_ERR_NOCONV;
+        } else if (!isfinite(alpha.x) || !isfinite(alpha.y) || !isfinite(beta.x) || !isfinite(beta.y)) {
+            cur.done = 1;
+            cur.iters = a.k;
+            cur.flag = DOT_ERR_BREAKDOWN;
+        } else {
+            sc.active = 1;
+            sc.alpha = alpha;
+            sc.beta = beta;
+            cur.rho_re = rho.x;
+            cur.rho_im = rho.y;
+            cur.alpha_re = alpha.x;
+            cur.alpha_im = alpha.y;
+        }
+    }
+    if (tile == 0) a.st[a.k & 1][rhs] = cur;
+    *out = sc;
+}
+
+// Plane coefficients of row n of A at plane k (R1-R3):
+//   theta [cx(2u - uW - uE) + cy(2u - uS - uN) + (mu + i shift) u] + cz(nzn u - uD - uU) + robin u
+struct PlaneCoef {
+    double thx, thy, th, dre, dim, wd, wu;
+};
+__device__ __forceinline__ PlaneCoef plane_coef(const OpConst& op, int k, double shift) {
+    PlaneCoef c;
+    const bool edge = (k == 0 || k == op.nz - 1);
+    c.th = edge ? 0.5 : 1.0;
+    c.thx = c.th * op.cx;
+    c.thy = c.th * op.cy;
+    c.dre = c.th * (2.0 * op.cx + 2.0 * op.cy) + op.cz * (edge ? 1.0 : 2.0) + (edge ? op.robin : 0.0);
+    c.dim = c.th * shift;
+    c.wd = k > 0 ? op.cz : 0.0;
+    c.wu = k < op.nz - 1 ? op.cz : 0.0;
+    return c;
+}
+
+__device__ __forceinline__ double2 stencil(const PlaneCoef& c, double mu, double2 u0, double2 sx, double2 sy,
+                                           double2 zd, double2 zu) {
+    const double dr = fma(c.th, mu, c.dre);
+    double2 r;
+    r.x = dr * u0.x - c.dim * u0.y - c.thx * sx.x - c.thy * sy.x - c.wd * zd.x - c.wu * zu.x;
+    r.y = dr * u0.y + c.dim * u0.x - c.thx * sx.y - c.thy * sy.y - c.wd * zd.y - c.wu * zu.y;
+    return r;
+}
+
+template <int I>
+struct IC {
+    static constexpr int v = I;
+};
+
+// Interior-plane stencil (theta = 1, both z-neighbours present): coefficients
+// straight from the kernel-parameter constant bank, no registers held.
+__device__ __forceinline__ double2 stencil_int(const OpConst& op, double shift, double mu, double2 u0, double2 sx,
+                                               double2 sy, double2 zs) {
+    const double dr = op.dint + mu;
+    double2 r;
+    r.x = dr * u0.x - shift * u0.y - op.cx * sx.x - op.cy * sy.x - op.cz * zs.x;
+    r.y = dr * u0.y + shift * u0.x - op.cx * sx.y - op.cy * sy.y - op.cz * zs.y;
+    return r;
+}
+
+// Slot layout (per ring slot): r [rowsP*nx] double2 | p [rowsP*nx] double2 | mu [rowsP*nx] double
+// (mu rides along in the same bulk-copy group when MUT; else it is loaded per thread).
+template <bool FULLX, int MAXT, int MINB, int NS, bool MUT>
+__global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int LPD = 4;                              // L2 prefetch distance (planes)
+    constexpr int PD = NS - 2;                          // TMA planes in flight
+    const int tile = blockIdx.x, rhs = blockIdx.y;
+    const int nx = a.op.nx, ny = a.op.ny, nz = a.op.nz;
+    const int TY = a.tl.TY;
+    const int ntiles = a.tl.ntiles;
+    const int rowsP = TY + 4, rowsR = TY + 2;
+    const int PS = nx * ny;
+    const size_t N = (size_t)PS * nz;
+    const int j0 = tile * TY;
+    const int slotE = rowsP * nx;                       // double2 elements of one vector in a slot
+    const int slotW = 2 * slotE + (MUT ? (slotE + 1) / 2 : 0);   // slot stride in double2
+    const int rbE = rowsR * nx;
+
+    double2* slots = reinterpret_cast<double2*>(smem_raw);          // [NS][slotW]
+    double2* rbuf = slots + (size_t)NS * slotW;                     // [3][rowsR*nx]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(rbuf + 3 * rbE);
+    double* scratch = reinterpret_cast<double*>(bars + NS);         // [32][kNumPartials]
+    __shared__ ZScalars sh_sc;
+
+    if (threadIdx.x < 32) zpass_scalars(a, rhs, tile, &sh_sc);
+    {   // zero the slot ring and Rbuf: rows outside the domain stay zero (Dirichlet y faces)
+        const int tot = NS * slotW + 3 * rbE;
+        for (int i = threadIdx.x; i < tot; i += blockDim.x) slots[i] = cmk(0, 0);
+    }
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < NS; ++q)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32z(&bars[q])), "r"(1));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (!sh_sc.active) return;
+    const bool first = (a.k == 0);
+    const double shift = a.shift[rhs];
+    const int kin = a.k & 1, kout = kin ^ 1;
+    const double2* __restrict__ Rin = a.R[kin] + (size_t)rhs * N;
+    const double2* __restrict__ Pin = a.Pv[kin] + (size_t)rhs * N;
+
+    // in-domain slot rows [rlo, rhi); grid row of slot row r is j0 - 2 + r
+    const int rlo = max(0, 2 - j0), rhi = min(rowsP, ny - j0 + 2);
+    const uint32_t tile_bytes = (uint32_t)((rhi - rlo) * nx * sizeof(double2));
+    const uint32_t mu_bytes = tile_bytes / 2;
+    const uint32_t tx_bytes = (first ? tile_bytes : 2 * tile_bytes) + (MUT ? mu_bytes : 0);
+    const int tile_off = (j0 - 2 + rlo) * nx;
+    const uint32_t slot0 = smem_u32z(slots + rlo * nx);             // r rows of slot 0
+    const uint32_t slot_stride = (uint32_t)(slotW * sizeof(double2));
+    const uint32_t pvec_off = (uint32_t)(slotE * sizeof(double2));
+    // mu rows land at slot + 2 slotE double2 + rlo*nx doubles (dR already includes rlo*nx double2)
+    const uint32_t mu_off = (uint32_t)(2 * slotE * sizeof(double2)) - (uint32_t)(rlo * nx * 8);
+    const uint32_t bar0 = smem_u32z(bars);
+
+    auto issue = [&](int z, int sl) {      // one thread: bulk copies of contiguous rows
+        const uint32_t dR = slot0 + sl * slot_stride, bar = bar0 + 8 * sl;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx_bytes) : "memory");
+        const size_t g = (size_t)z * PS + tile_off;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dR),
+            "l"(Rin + g), "r"(tile_bytes), "r"(bar)
+            : "memory");
+        if (!first)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    dR + pvec_off),
+                "l"(Pin + g), "r"(tile_bytes), "r"(bar)
+                : "memory");
+        if (MUT)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    dR + mu_off),
+                "l"(a.mu + g), "r"(mu_bytes), "r"(bar)
+                : "memory");
+    };
+    auto prefetch_l2 = [&](int z) {
+        const size_t g = (size_t)z * PS + tile_off;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Rin + g), "r"(tile_bytes) : "memory");
+        if (!first)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Pin + g), "r"(tile_bytes) : "memory");
+    };
+    if (threadIdx.x == 0)
+        for (int z = 0; z < PD && z < nz; ++z) issue(z, z);
+    if (threadIdx.x == 32)
+        for (int z = PD; z < PD + LPD && z < nz; ++z) prefetch_l2(z);
+
+    // ---- per-thread geometry
+    const int t = threadIdx.x;
+    const int r = t / nx, x = t - r * nx;              // slot row, column
+    const int grow = j0 - 2 + r;                       // grid row
+    const bool indom = r < rowsP && r >= rlo && r < rhi;
+    const bool own = indom && r >= 2 && r < TY + 2;
+    const bool h1 = indom && (r == 1 || r == TY + 2);
+    const bool ph2 = own || h1;
+    const int o = r * nx + x;                          // slot element
+    const int o3 = (r - 1) * nx + x;                   // Rbuf element
+    const int go = indom ? grow * nx + x : 0;          // offset in a plane
+    const bool hasW = x > 0, hasE = x < nx - 1;
+    // running per-thread global pointers (advance one plane per step)
+    double2* pP = a.Pv[kout] + (size_t)rhs * N + go;                       // p_k at plane f
+    double2* pR = a.R[kout] + (size_t)rhs * N + go - 2 * (ptrdiff_t)PS;    // r_{k+1} at plane f - 2
+    double2* pX = FULLX ? a.X + (size_t)rhs * N + go : nullptr;
+    const double* pMu = a.mu + go;                     // used when !MUT
+
+    double acc[kNumPartials];
+#pragma unroll
+    for (int q = 0; q < kNumPartials; ++q) acc[q] = 0.0;
+
+    const double2 z2 = cmk(0, 0);
+    double2 Pq[3] = {z2, z2, z2};      // p_k at planes == index mod 3 (own column)
+    double2 RN[3] = {z2, z2, z2};      // r_{k+1}
+    double MU[3] = {0.0, 0.0, 0.0};    // mu (only when !MUT)
+    double mu_carry = 0.0;             // mu at plane f - 2 (phase 3), taken from phase 2 of step f - 1
+    const int32_t* soff = a.samp_off + tile;
+    int sl = 0;                        // ring slot of plane f
+    uint32_t par = 0;                  // mbarrier parity of plane f
+    int sl_prev = NS - 1;              // ring slot of plane f - 1
+    int sl_iss = PD % NS;              // ring slot of plane f + PD
+
+    auto step = [&](int f, auto IDX) {
+        constexpr int i0 = decltype(IDX)::v;           // f % 3
+        constexpr int i1 = (i0 + 2) % 3;               // (f - 1) % 3
+        constexpr int i2 = (i0 + 1) % 3;               // (f - 2) % 3
+        if (threadIdx.x == 0 && f + PD < nz) issue(f + PD, sl_iss);
+        if (threadIdx.x == 32 && f + PD + LPD < nz) prefetch_l2(f + PD + LPD);
+        if (!MUT && ph2 && f < nz) MU[i0] = pMu[(size_t)f * PS];
+        // ---- phase 1: plane f
+        double2 pf = z2;
+        if (f < nz) {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "WAITZ_%=:\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                "@!p bra WAITZ_%=;\n\t}" ::"r"(bar0 + 8 * sl),
+                "r"(par)
+                : "memory");
+            if (indom) {
+                double2* sr = slots + sl * slotW;
+                const double2 rf = sr[o];
+                pf = first ? rf : cfma(sh_sc.beta, sr[slotE + o], rf);
+                sr[slotE + o] = pf;
+                if (own) {
+                    *pP = pf;
+                    if (FULLX) *pX = cfma(sh_sc.alpha, pf, *pX);
+                }
+            }
+        }
+        Pq[i0] = pf;
+        // ---- phase 2: plane g = f - 1
+        double2 rng = z2;
+        double mug = 0.0;
+        const int g = f - 1;
+        if (g >= 0 && g < nz) {
+            const double2* sr = slots + sl_prev * slotW;
+            const double2* sp = sr + slotE;
+            if (ph2) {
+                const double2 xw = hasW ? sp[o - 1] : z2;
+                const double2 xe = hasE ? sp[o + 1] : z2;
+                const double2 ys = sp[o - nx], yn = sp[o + nx];
+                mug = MUT ? reinterpret_cast<const double*>(sr + 2 * slotE)[o] : MU[i1];
+                const double2 pc = Pq[i1];
+                double2 qv;
+                if (g > 0 && g < nz - 1)
+                    qv = stencil_int(a.op, shift, mug, pc, cadd(xw, xe), cadd(ys, yn), cadd(Pq[i2], pf));
+                else
+                    qv = stencil(plane_coef(a.op, g, shift), mug, pc, cadd(xw, xe), cadd(ys, yn), Pq[i2], pf);
+                const double2 alpha = sh_sc.alpha;
+                rng = csub(sr[o], cmul(alpha, qv));
+                rbuf[i1 * rbE + o3] = rng;
+                if (own) {
+                    acc[4] = fma(rng.x, qv.x, fma(-rng.y, qv.y, acc[4]));
+                    acc[5] = fma(rng.x, qv.y, fma(rng.y, qv.x, acc[5]));
+                    acc[6] = fma(pc.x, qv.x, fma(-pc.y, qv.y, acc[6]));
+                    acc[7] = fma(pc.x, qv.y, fma(pc.y, qv.x, acc[7]));
+                }
+            }
+            if (!FULLX && a.nP > 0) {
+                const int s0 = soff[g * ntiles], s1 = soff[g * ntiles + 1];
+                if (s0 < s1) {
+                    double2* XP = a.XP + (size_t)rhs * a.nP;
+                    for (int si = s0 + threadIdx.x; si < s1; si += blockDim.x) {
+                        const int rem = a.samp_nodes[si] - g * PS;
+                        XP[si] = cfma(sh_sc.alpha, sp[rem - (j0 - 2) * nx], XP[si]);
+                    }
+                }
+            }
+        }
+        // ---- phase 3: plane tt = f - 2
+        const int tt = f - 2;
+        if (own && tt >= 0) {
+            const double2* rc = rbuf + i2 * rbE;
+            const double2 xw = hasW ? rc[o3 - 1] : z2;
+            const double2 xe = hasE ? rc[o3 + 1] : z2;
+            const double2 ys = rc[o3 - nx], yn = rc[o3 + nx];
+            const double2 r0 = RN[i2];
+            // the slot of plane f - 2 is being refilled by this step's bulk copy: mu comes
+            // from the register carried over from phase 2 of the previous step
+            const double mut = MUT ? mu_carry : MU[i2];
+            double2 ar;
+            if (tt > 0 && tt < nz - 1)
+                ar = stencil_int(a.op, shift, mut, r0, cadd(xw, xe), cadd(ys, yn), cadd(RN[i0], rng));
+            else
+                ar = stencil(plane_coef(a.op, tt, shift), mut, r0, cadd(xw, xe), cadd(ys, yn), RN[i0], rng);
+            acc[0] = fma(r0.x, r0.x, fma(-r0.y, r0.y, acc[0]));
+            acc[1] = fma(2.0 * r0.x, r0.y, acc[1]);
+            acc[2] = fma(r0.x, ar.x, fma(-r0.y, ar.y, acc[2]));
+            acc[3] = fma(r0.x, ar.y, fma(r0.y, ar.x, acc[3]));
+            acc[8] = fma(r0.x, r0.x, fma(r0.y, r0.y, acc[8]));
+            *pR = r0;
+        }
+        RN[i1] = rng;
+        mu_carry = mug;
+        pP += PS;
+        pR += PS;
+        if (FULLX) pX += PS;
+        sl_prev = sl;
+        if (++sl == NS) {
+            sl = 0;
+            par ^= 1u;
+        }
+        if (++sl_iss == NS) sl_iss = 0;
+        __syncthreads();
+    };
+    // RN[i0] read in phase 3 is r_{k+1}(f-3), written three steps earlier.
+#pragma unroll 1
+    for (int f = 0; f < nz + 2; f += 3) {
+        step(f, IC<0>());
+        if (f + 1 < nz + 2) step(f + 1, IC<1>());
+        if (f + 2 < nz + 2) step(f + 2, IC<2>());
+    }
+    // ---- deterministic block reduction of the partials
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int i = 0; i < kNumPartials; ++i) acc[i] = warp_sum_z(acc[i]);
+    if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < kNumPartials; ++i) scratch[warp * kNumPartials + i] = acc[i];
+    __syncthreads();
+    if (threadIdx.x < kNumPartials) {
+        double sum = 0;
+        for (int w = 0; w < nw; ++w) sum += scratch[w * kNumPartials + threadIdx.x];
+        a.part[kout][((size_t)rhs * ntiles + tile) * kNumPartials + threadIdx.x] = sum;
+    }
+}
+
+template <bool FX, int MAXT, int MINB, int NS>
+void launch_z_ns(const PassArgs& a, int nb, cudaStream_t s) {
+    // mu rides in the bulk-copy group when every copy is 16-byte sized and aligned
+    const bool mut = (a.op.nx % 2 == 0);
+    auto k = mut ? cocg_zpass_kernel<FX, MAXT, MINB, NS, true> : cocg_zpass_kernel<FX, MAXT, MINB, NS, false>;
+    static size_t attr[2] = {0, 0};
+    if (attr[mut] < a.tl.smem) {
+        DOT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.tl.smem));
+        attr[mut] = a.tl.smem;
+    }
+    dim3 grid(a.tl.ntiles, nb);
+    launch_clustered(k, grid, a.tl.threads, a.tl.smem, s, a.tl.cluster, a);
+}
+
+template <bool FX, int MAXT, int MINB>
+void launch_z(const PassArgs& a, int nb, cudaStream_t s) {
+    switch (a.tl.nslots) {
+        case 3: launch_z_ns<FX, MAXT, MINB, 3>(a, nb, s); break;
+        case 4: launch_z_ns<FX, MAXT, MINB, 4>(a, nb, s); break;
+        case 5: launch_z_ns<FX, MAXT, MINB, 5>(a, nb, s); break;
+        default: throw Error(DOT_ERR_ARG, "z pass supports 3..5 ring slots (DOT_COCG_PREFETCH 1..3)");
+    }
+}
+
+}  // namespace
+
+size_t zpass_smem(int nx, int TY, int NS) {
+    const size_t slotE = (size_t)(TY + 4) * nx;
+    const size_t e = (size_t)NS * (2 * slotE + (nx % 2 == 0 ? (slotE + 1) / 2 : 0)) + 3 * (size_t)(TY + 2) * nx;
+    return e * sizeof(double2) + NS * 8 + 32 * kNumPartials * 8 + 128;
+}
+
+void launch_cocg_zpass(const PassArgs& a, int nb, cudaStream_t s) {
+    const int maxt = a.tl.threads;
+    if (a.X) {
+        if (maxt <= 512) launch_z<true, 512, 1>(a, nb, s);
+        else launch_z<true, 1024, 1>(a, nb, s);
+        return;
+    }
+    if (a.tl.minb >= 2) launch_z<false, 512, 2>(a, nb, s);
+    else if (maxt <= 512) launch_z<false, 512, 1>(a, nb, s);
+    else if (maxt <= 768) launch_z<false, 768, 1>(a, nb, s);
+    else launch_z<false, 1024, 1>(a, nb, s);
+}
+
+}  // namespace dot

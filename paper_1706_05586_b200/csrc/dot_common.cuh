@@ -54,6 +54,7 @@ __host__ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
 struct OpConst {
     int nx, ny, nz;
     double cx, cy, cz, robin;   // D/hx^2, D/hy^2, D/hz^2, 1/(2 hz)
+    double dint;                // interior-plane diagonal without mu: 2 cx + 2 cy + 2 cz
 };
 
 __device__ __forceinline__ double theta_of(int k, int nz) { return (k == 0 || k == nz - 1) ? 0.5 : 1.0; }

@@ -10,12 +10,18 @@ namespace dot {
 // marches all nz planes; planes (with a 2-row y halo) are staged by TMA bulk
 // copies into a ring of `nslots` shared-memory slots.
 struct CocgTiling {
+    int kind = 1;         // 1: z-register pass (cocg_z.cu), 0: padded-ring pass (cocg.cu)
+    int cluster = 1;      // thread-block cluster size along the tiles of one RHS (divides ntiles)
+    int minb = 1;         // CTAs per SM the z pass is compiled for
     int TY = 0, ntiles = 0, nslots = 0, threads = 512;
     int rpt = 0;          // x-rows covered by one sweep of the block (threads = roundup32(nx * rpt))
     size_t smem = 0;
 };
 // prefetch: planes loaded ahead (slots = prefetch + 3); max_smem: per-CTA budget (bytes)
-CocgTiling cocg_tiling(int nx, int ny, int nz, int prefetch = 1, size_t max_smem = 0, int max_threads = 0);
+// kind: 1 = z-register pass if a tiling fits (else the ring pass), 0 = ring pass;
+// want_ty > 0 forces the z-pass tile height.
+CocgTiling cocg_tiling(int nx, int ny, int nz, int prefetch = 1, size_t max_smem = 0, int max_threads = 0,
+                       int kind = 1, int want_ty = 0);
 
 struct PassArgs {
     OpConst op;
@@ -36,6 +42,33 @@ struct PassArgs {
     double2* X = nullptr;                 // [nb][N] full solution (test mode) or null
 };
 
+// Launch a pass kernel, as a thread-block cluster of `cs` consecutive tiles of one
+// RHS when cs > 1 (co-scheduled, so y-halo rows read by neighbours hit in L2).
+template <class K>
+void launch_clustered(K kernel, dim3 grid, int threads, size_t smem, cudaStream_t s, int cs, const PassArgs& a) {
+    if (cs <= 1) {
+        kernel<<<grid, threads, smem, s>>>(a);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        DOT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, a));
+    }
+    DOT_CUDA_TRY(cudaGetLastError());
+}
+
+// z-register pass (cocg_z.cu)
+size_t zpass_smem(int nx, int TY, int NS);
+void launch_cocg_zpass(const PassArgs& a, int nb, cudaStream_t s);
 void launch_cocg_init(const PassArgs& a, int nb, cudaStream_t s);
 void launch_cocg_pass(const PassArgs& a, int nb, cudaStream_t s);
 void launch_count_active(const RhsState* st, int nb, int* d_count, cudaStream_t s);

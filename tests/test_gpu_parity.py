@@ -237,9 +237,17 @@ def test_optimize_directions_parity(dot):
         assert np.allclose(np.linalg.norm(Wg[:, -1]), 3.0)
 
 
-@pytest.mark.parametrize("knobs", [dict(DOT_COCG_THREADS="256"), dict(DOT_COCG_THREADS="128"),
-                                   dict(DOT_COCG_SMEM_KB="64"), dict(DOT_COCG_PREFETCH="2"),
-                                   dict(DOT_COCG_THREADS="256", DOT_COCG_SMEM_KB="110")])
+RING = dict(DOT_COCG_KERNEL="ring")
+KNOBS = [dict(RING, DOT_COCG_THREADS="256"), dict(RING, DOT_COCG_THREADS="128"),
+         dict(RING, DOT_COCG_SMEM_KB="64"), dict(RING, DOT_COCG_PREFETCH="2"),
+         dict(RING, DOT_COCG_THREADS="256", DOT_COCG_SMEM_KB="110"),
+         # z-register pass: every thread-count option, ring depth, tile height and clusters
+         dict(DOT_COCG_ZOPT="A"), dict(DOT_COCG_ZOPT="B"), dict(DOT_COCG_ZOPT="C"),
+         dict(DOT_COCG_PREFETCH="1"), dict(DOT_COCG_PREFETCH="3"), dict(DOT_COCG_TY="3"), dict(DOT_COCG_TY="5"),
+         dict(DOT_COCG_TY="4", DOT_COCG_CLUSTER="2")]
+
+
+@pytest.mark.parametrize("knobs", KNOBS)
 def test_tiling_knobs_keep_parity(dot, knobs, monkeypatch):
     """Every tiling the run-time knobs can select solves the same systems
     (guards the generic kernel instance and the tiling constraints)."""
