@@ -496,17 +496,18 @@ static CocgTiling ring_tiling(int nx, int ny, int nz, int prefetch, size_t max_s
     return t;
 }
 
-// z-register pass tiling (cocg_z.cu): one thread per (x, slot row) of TY + 4 rows.
-// Options in order of preference (measured on B200 at 64^3):
-//   B: <= 768 threads, one CTA per SM (78 registers, no spills)
-//   C: <= 1024 threads (64 registers)      A: <= 512 threads, two CTAs per SM (64 registers)
+// z-register pass tiling (cocg_z.cu): a thread owns `rows` slot rows of one column
+// of the TY + 4 slot rows.  Options in order of preference:
+//   D: 2 rows per thread, <= 512 threads, one CTA per SM
+//   B: 1 row per thread, <= 768 threads, one CTA per SM (78 registers, no spills)
+//   C: 1 row, <= 1024 threads (64 registers)     A: 1 row, <= 512 threads, two CTAs per SM
 // The first option whose tile height reaches 4 rows wins, else the one with the largest TY.
-// DOT_COCG_ZOPT=A|B|C forces one option.
-static bool z_tiling(int nx, int ny, int prefetch, int want_ty, CocgTiling& out) {
+// DOT_COCG_ZOPT=A|B|C|D forces one option.
+static bool z_tiling(int nx, int ny, int nz, int prefetch, int want_ty, CocgTiling& out) {
     const int NS = prefetch + 2;
     const size_t sm_cta = 227 * 1024, sm_sm = 228 * 1024 - 2048;
-    struct Opt { char name; int maxt, minb; };
-    const Opt opts[3] = {{'B', 768, 1}, {'C', 1024, 1}, {'A', 512, 2}};
+    struct Opt { char name; int rows, maxt, minb; };
+    const Opt opts[4] = {{'D', 2, 512, 1}, {'B', 1, 768, 1}, {'C', 1, 1024, 1}, {'A', 1, 512, 2}};
     const char* eO = std::getenv("DOT_COCG_ZOPT");
     CocgTiling best;
     bool found = false;
@@ -514,8 +515,8 @@ static bool z_tiling(int nx, int ny, int prefetch, int want_ty, CocgTiling& out)
         if (eO && eO[0] != o.name) continue;
         int ty = 0;
         for (int c = 1; c <= ny; ++c) {
-            const int thr = ((c + 4) * nx + 31) / 32 * 32;
-            const size_t sm = zpass_smem(nx, c, NS);
+            const int thr = ((c + 4 + o.rows - 1) / o.rows * nx + 31) / 32 * 32;
+            const size_t sm = zpass_smem(nx, c, NS, nz);
             if (thr > o.maxt || sm > sm_cta || (size_t)o.minb * (sm + 1024) > sm_sm) break;
             ty = c;
             if (want_ty > 0 && c == want_ty) break;
@@ -526,11 +527,12 @@ static bool z_tiling(int nx, int ny, int prefetch, int want_ty, CocgTiling& out)
         CocgTiling t;
         t.kind = 1;
         t.minb = o.minb;
+        t.zrows = o.rows;
         t.TY = (ny + ntiles - 1) / ntiles;
         t.ntiles = (ny + t.TY - 1) / t.TY;
         t.nslots = NS;
-        t.threads = ((t.TY + 4) * nx + 31) / 32 * 32;
-        t.smem = zpass_smem(nx, t.TY, NS);
+        t.threads = ((t.TY + 4 + o.rows - 1) / o.rows * nx + 31) / 32 * 32;
+        t.smem = zpass_smem(nx, t.TY, NS, nz);
         if (!found || (best.TY < 4 && t.TY > best.TY)) {
             best = t;
             found = true;
@@ -545,7 +547,7 @@ CocgTiling cocg_tiling(int nx, int ny, int nz, int prefetch, size_t max_smem, in
                        int want_ty) {
     if (kind != 0) {
         CocgTiling t;
-        if (z_tiling(nx, ny, std::max(1, prefetch), want_ty, t)) return t;
+        if (z_tiling(nx, ny, nz, std::max(1, std::min(prefetch, 2)), want_ty, t)) return t;
         if (kind == 1 && want_ty > 0) throw Error(DOT_ERR_ARG, "requested z-pass tile height does not fit");
     }
     return ring_tiling(nx, ny, nz, std::max(1, prefetch - (kind != 0 ? 1 : 0)), max_smem, max_threads);

@@ -145,7 +145,9 @@ __device__ __forceinline__ double2 stencil_int(const OpConst& op, double shift, 
 
 // Slot layout (per ring slot): r [rowsP*nx] double2 | p [rowsP*nx] double2 | mu [rowsP*nx] double
 // (mu rides along in the same bulk-copy group when MUT; else it is loaded per thread).
-template <bool FULLX, int MAXT, int MINB, int NS, bool MUT>
+// RPT: slot rows per thread (a thread owns rows RPT*m .. RPT*m + RPT - 1 of one column; the
+// y-neighbours inside its strip come from registers).
+template <bool FULLX, int MAXT, int MINB, int NS, bool MUT, int RPT>
 __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int LPD = 4;                              // L2 prefetch distance (planes)
@@ -166,12 +168,16 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
     double2* rbuf = slots + (size_t)NS * slotW;                     // [3][rowsR*nx]
     uint64_t* bars = reinterpret_cast<uint64_t*>(rbuf + 3 * rbE);
     double* scratch = reinterpret_cast<double*>(bars + NS);         // [32][kNumPartials]
+    int2* s_samp = reinterpret_cast<int2*>(scratch + 32 * kNumPartials);   // [nz] sample ranges
     __shared__ ZScalars sh_sc;
 
     if (threadIdx.x < 32) zpass_scalars(a, rhs, tile, &sh_sc);
     {   // zero the slot ring and Rbuf: rows outside the domain stay zero (Dirichlet y faces)
         const int tot = NS * slotW + 3 * rbE;
         for (int i = threadIdx.x; i < tot; i += blockDim.x) slots[i] = cmk(0, 0);
+        if (!FULLX && a.nP > 0)
+            for (int g = threadIdx.x; g < nz; g += blockDim.x)
+                s_samp[g] = make_int2(a.samp_off[g * ntiles + tile], a.samp_off[g * ntiles + tile + 1]);
     }
     if (threadIdx.x == 0) {
         for (int q = 0; q < NS; ++q)
@@ -232,17 +238,25 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
     if (threadIdx.x == 32)
         for (int z = PD; z < PD + LPD && z < nz; ++z) prefetch_l2(z);
 
-    // ---- per-thread geometry
+    // ---- per-thread geometry: rows r0 .. r0 + RPT - 1 of column x
     const int t = threadIdx.x;
-    const int r = t / nx, x = t - r * nx;              // slot row, column
-    const int grow = j0 - 2 + r;                       // grid row
-    const bool indom = r < rowsP && r >= rlo && r < rhi;
-    const bool own = indom && r >= 2 && r < TY + 2;
-    const bool h1 = indom && (r == 1 || r == TY + 2);
-    const bool ph2 = own || h1;
-    const int o = r * nx + x;                          // slot element
-    const int o3 = (r - 1) * nx + x;                   // Rbuf element
-    const int go = indom ? grow * nx + x : 0;          // offset in a plane
+    const int m = t / nx, x = t - m * nx;
+    const int r0 = RPT * m;
+    bool indom[RPT], own[RPT], ph2[RPT];
+    bool any_in = false, any2 = false, any_own = false;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+        const int r = r0 + j;
+        indom[j] = r < rowsP && r >= rlo && r < rhi;
+        own[j] = indom[j] && r >= 2 && r < TY + 2;
+        ph2[j] = own[j] || (indom[j] && (r == 1 || r == TY + 2));
+        any_in |= indom[j];
+        any2 |= ph2[j];
+        any_own |= own[j];
+    }
+    const int o = r0 * nx + x;                         // slot element of row 0
+    const int o3 = o - nx;                             // Rbuf element of row 0
+    const int go = (j0 - 2 + r0) * nx + x;             // plane offset of row 0 (may be outside; unused then)
     const bool hasW = x > 0, hasE = x < nx - 1;
     // running per-thread global pointers (advance one plane per step)
     double2* pP = a.Pv[kout] + (size_t)rhs * N + go;                       // p_k at plane f
@@ -255,11 +269,18 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
     for (int q = 0; q < kNumPartials; ++q) acc[q] = 0.0;
 
     const double2 z2 = cmk(0, 0);
-    double2 Pq[3] = {z2, z2, z2};      // p_k at planes == index mod 3 (own column)
-    double2 RN[3] = {z2, z2, z2};      // r_{k+1}
-    double MU[3] = {0.0, 0.0, 0.0};    // mu (only when !MUT)
-    double mu_carry = 0.0;             // mu at plane f - 2 (phase 3), taken from phase 2 of step f - 1
-    const int32_t* soff = a.samp_off + tile;
+    double2 Pq[RPT][3], RN[RPT][3];    // p_k, r_{k+1} at planes == index mod 3 (own column)
+    double MU[RPT][3], mu_carry[RPT];  // mu (register pipeline only when !MUT); mu of plane f - 2
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            Pq[j][q] = z2;
+            RN[j][q] = z2;
+            MU[j][q] = 0.0;
+        }
+        mu_carry[j] = 0.0;
+    }
     int sl = 0;                        // ring slot of plane f
     uint32_t par = 0;                  // mbarrier parity of plane f
     int sl_prev = NS - 1;              // ring slot of plane f - 1
@@ -271,9 +292,14 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
         constexpr int i2 = (i0 + 1) % 3;               // (f - 2) % 3
         if (threadIdx.x == 0 && f + PD < nz) issue(f + PD, sl_iss);
         if (threadIdx.x == 32 && f + PD + LPD < nz) prefetch_l2(f + PD + LPD);
-        if (!MUT && ph2 && f < nz) MU[i0] = pMu[(size_t)f * PS];
+        if (!MUT && f < nz)
+#pragma unroll
+            for (int j = 0; j < RPT; ++j)
+                if (ph2[j]) MU[j][i0] = pMu[(size_t)f * PS + j * nx];
         // ---- phase 1: plane f
-        double2 pf = z2;
+        double2 pf[RPT];
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) pf[j] = z2;
         if (f < nz) {
             asm volatile(
                 "{\n\t.reg .pred p;\n\t"
@@ -282,82 +308,110 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
                 "@!p bra WAITZ_%=;\n\t}" ::"r"(bar0 + 8 * sl),
                 "r"(par)
                 : "memory");
-            if (indom) {
-                double2* sr = slots + sl * slotW;
-                const double2 rf = sr[o];
-                pf = first ? rf : cfma(sh_sc.beta, sr[slotE + o], rf);
-                sr[slotE + o] = pf;
-                if (own) {
-                    *pP = pf;
-                    if (FULLX) *pX = cfma(sh_sc.alpha, pf, *pX);
+            if (any_in) {
+                double2* sr = slots + sl * slotW + o;
+                const double2 beta = sh_sc.beta;
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) {
+                    if (!indom[j]) continue;
+                    const double2 rf = sr[j * nx];
+                    pf[j] = first ? rf : cfma(beta, sr[slotE + j * nx], rf);
+                    sr[slotE + j * nx] = pf[j];
+                    if (own[j]) {
+                        pP[j * nx] = pf[j];
+                        if (FULLX) pX[j * nx] = cfma(sh_sc.alpha, pf[j], pX[j * nx]);
+                    }
                 }
             }
         }
-        Pq[i0] = pf;
         // ---- phase 2: plane g = f - 1
-        double2 rng = z2;
-        double mug = 0.0;
+        double2 rng[RPT];
+        double mug[RPT];
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            rng[j] = z2;
+            mug[j] = 0.0;
+        }
         const int g = f - 1;
         if (g >= 0 && g < nz) {
             const double2* sr = slots + sl_prev * slotW;
             const double2* sp = sr + slotE;
-            if (ph2) {
-                const double2 xw = hasW ? sp[o - 1] : z2;
-                const double2 xe = hasE ? sp[o + 1] : z2;
-                const double2 ys = sp[o - nx], yn = sp[o + nx];
-                mug = MUT ? reinterpret_cast<const double*>(sr + 2 * slotE)[o] : MU[i1];
-                const double2 pc = Pq[i1];
-                double2 qv;
-                if (g > 0 && g < nz - 1)
-                    qv = stencil_int(a.op, shift, mug, pc, cadd(xw, xe), cadd(ys, yn), cadd(Pq[i2], pf));
-                else
-                    qv = stencil(plane_coef(a.op, g, shift), mug, pc, cadd(xw, xe), cadd(ys, yn), Pq[i2], pf);
+            if (any2) {
+                const bool interior = g > 0 && g < nz - 1;
+                const PlaneCoef ce = interior ? PlaneCoef{} : plane_coef(a.op, g, shift);
                 const double2 alpha = sh_sc.alpha;
-                rng = csub(sr[o], cmul(alpha, qv));
-                rbuf[i1 * rbE + o3] = rng;
-                if (own) {
-                    acc[4] = fma(rng.x, qv.x, fma(-rng.y, qv.y, acc[4]));
-                    acc[5] = fma(rng.x, qv.y, fma(rng.y, qv.x, acc[5]));
-                    acc[6] = fma(pc.x, qv.x, fma(-pc.y, qv.y, acc[6]));
-                    acc[7] = fma(pc.x, qv.y, fma(pc.y, qv.x, acc[7]));
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) {
+                    if (!ph2[j]) continue;
+                    const int oj = o + j * nx;
+                    const double2 xw = hasW ? sp[oj - 1] : z2;
+                    const double2 xe = hasE ? sp[oj + 1] : z2;
+                    const double2 ys = j > 0 ? Pq[j > 0 ? j - 1 : 0][i1] : sp[oj - nx];
+                    const double2 yn = j < RPT - 1 ? Pq[j < RPT - 1 ? j + 1 : 0][i1] : sp[oj + nx];
+                    mug[j] = MUT ? reinterpret_cast<const double*>(sr + 2 * slotE)[oj] : MU[j][i1];
+                    const double2 pc = Pq[j][i1];
+                    double2 qv;
+                    if (interior)
+                        qv = stencil_int(a.op, shift, mug[j], pc, cadd(xw, xe), cadd(ys, yn), cadd(Pq[j][i2], pf[j]));
+                    else
+                        qv = stencil(ce, mug[j], pc, cadd(xw, xe), cadd(ys, yn), Pq[j][i2], pf[j]);
+                    rng[j] = csub(sr[oj], cmul(alpha, qv));
+                    rbuf[i1 * rbE + o3 + j * nx] = rng[j];
+                    if (own[j]) {
+                        acc[4] = fma(rng[j].x, qv.x, fma(-rng[j].y, qv.y, acc[4]));
+                        acc[5] = fma(rng[j].x, qv.y, fma(rng[j].y, qv.x, acc[5]));
+                        acc[6] = fma(pc.x, qv.x, fma(-pc.y, qv.y, acc[6]));
+                        acc[7] = fma(pc.x, qv.y, fma(pc.y, qv.x, acc[7]));
+                    }
                 }
             }
             if (!FULLX && a.nP > 0) {
-                const int s0 = soff[g * ntiles], s1 = soff[g * ntiles + 1];
-                if (s0 < s1) {
+                const int2 sr2 = s_samp[g];
+                if (sr2.x < sr2.y) {
                     double2* XP = a.XP + (size_t)rhs * a.nP;
-                    for (int si = s0 + threadIdx.x; si < s1; si += blockDim.x) {
+                    for (int si = sr2.x + threadIdx.x; si < sr2.y; si += blockDim.x) {
                         const int rem = a.samp_nodes[si] - g * PS;
                         XP[si] = cfma(sh_sc.alpha, sp[rem - (j0 - 2) * nx], XP[si]);
                     }
                 }
             }
         }
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) Pq[j][i0] = pf[j];
         // ---- phase 3: plane tt = f - 2
         const int tt = f - 2;
-        if (own && tt >= 0) {
-            const double2* rc = rbuf + i2 * rbE;
-            const double2 xw = hasW ? rc[o3 - 1] : z2;
-            const double2 xe = hasE ? rc[o3 + 1] : z2;
-            const double2 ys = rc[o3 - nx], yn = rc[o3 + nx];
-            const double2 r0 = RN[i2];
-            // the slot of plane f - 2 is being refilled by this step's bulk copy: mu comes
-            // from the register carried over from phase 2 of the previous step
-            const double mut = MUT ? mu_carry : MU[i2];
-            double2 ar;
-            if (tt > 0 && tt < nz - 1)
-                ar = stencil_int(a.op, shift, mut, r0, cadd(xw, xe), cadd(ys, yn), cadd(RN[i0], rng));
-            else
-                ar = stencil(plane_coef(a.op, tt, shift), mut, r0, cadd(xw, xe), cadd(ys, yn), RN[i0], rng);
-            acc[0] = fma(r0.x, r0.x, fma(-r0.y, r0.y, acc[0]));
-            acc[1] = fma(2.0 * r0.x, r0.y, acc[1]);
-            acc[2] = fma(r0.x, ar.x, fma(-r0.y, ar.y, acc[2]));
-            acc[3] = fma(r0.x, ar.y, fma(r0.y, ar.x, acc[3]));
-            acc[8] = fma(r0.x, r0.x, fma(r0.y, r0.y, acc[8]));
-            *pR = r0;
+        if (any_own && tt >= 0) {
+            const double2* rc = rbuf + i2 * rbE + o3;
+            const bool interior = tt > 0 && tt < nz - 1;
+            const PlaneCoef ce = interior ? PlaneCoef{} : plane_coef(a.op, tt, shift);
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) {
+                if (!own[j]) continue;
+                const double2 xw = hasW ? rc[j * nx - 1] : z2;
+                const double2 xe = hasE ? rc[j * nx + 1] : z2;
+                // y-neighbours: own-strip rows from registers (r_{k+1} of plane tt is RN[.][i2])
+                const double2 ys = j > 0 ? RN[j > 0 ? j - 1 : 0][i2] : rc[(j - 1) * nx];
+                const double2 yn = j < RPT - 1 ? RN[j < RPT - 1 ? j + 1 : 0][i2] : rc[(j + 1) * nx];
+                const double2 r0v = RN[j][i2];
+                const double mut = MUT ? mu_carry[j] : MU[j][i2];
+                double2 ar;
+                if (interior)
+                    ar = stencil_int(a.op, shift, mut, r0v, cadd(xw, xe), cadd(ys, yn), cadd(RN[j][i0], rng[j]));
+                else
+                    ar = stencil(ce, mut, r0v, cadd(xw, xe), cadd(ys, yn), RN[j][i0], rng[j]);
+                acc[0] = fma(r0v.x, r0v.x, fma(-r0v.y, r0v.y, acc[0]));
+                acc[1] = fma(2.0 * r0v.x, r0v.y, acc[1]);
+                acc[2] = fma(r0v.x, ar.x, fma(-r0v.y, ar.y, acc[2]));
+                acc[3] = fma(r0v.x, ar.y, fma(r0v.y, ar.x, acc[3]));
+                acc[8] = fma(r0v.x, r0v.x, fma(r0v.y, r0v.y, acc[8]));
+                pR[j * nx] = r0v;
+            }
         }
-        RN[i1] = rng;
-        mu_carry = mug;
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            RN[j][i1] = rng[j];
+            mu_carry[j] = mug[j];
+        }
         pP += PS;
         pR += PS;
         if (FULLX) pX += PS;
@@ -369,7 +423,7 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
         if (++sl_iss == NS) sl_iss = 0;
         __syncthreads();
     };
-    // RN[i0] read in phase 3 is r_{k+1}(f-3), written three steps earlier.
+    // RN[.][i0] read in phase 3 is r_{k+1}(f-3), written three steps earlier.
 #pragma unroll 1
     for (int f = 0; f < nz + 2; f += 3) {
         step(f, IC<0>());
@@ -391,11 +445,11 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
     }
 }
 
-template <bool FX, int MAXT, int MINB, int NS>
+template <bool FX, int MAXT, int MINB, int NS, int RPT>
 void launch_z_ns(const PassArgs& a, int nb, cudaStream_t s) {
     // mu rides in the bulk-copy group when every copy is 16-byte sized and aligned
     const bool mut = (a.op.nx % 2 == 0);
-    auto k = mut ? cocg_zpass_kernel<FX, MAXT, MINB, NS, true> : cocg_zpass_kernel<FX, MAXT, MINB, NS, false>;
+    auto k = mut ? cocg_zpass_kernel<FX, MAXT, MINB, NS, true, RPT> : cocg_zpass_kernel<FX, MAXT, MINB, NS, false, RPT>;
     static size_t attr[2] = {0, 0};
     if (attr[mut] < a.tl.smem) {
         DOT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.tl.smem));
@@ -405,35 +459,40 @@ void launch_z_ns(const PassArgs& a, int nb, cudaStream_t s) {
     launch_clustered(k, grid, a.tl.threads, a.tl.smem, s, a.tl.cluster, a);
 }
 
-template <bool FX, int MAXT, int MINB>
+template <bool FX, int MAXT, int MINB, int RPT>
 void launch_z(const PassArgs& a, int nb, cudaStream_t s) {
     switch (a.tl.nslots) {
-        case 3: launch_z_ns<FX, MAXT, MINB, 3>(a, nb, s); break;
-        case 4: launch_z_ns<FX, MAXT, MINB, 4>(a, nb, s); break;
-        case 5: launch_z_ns<FX, MAXT, MINB, 5>(a, nb, s); break;
-        default: throw Error(DOT_ERR_ARG, "z pass supports 3..5 ring slots (DOT_COCG_PREFETCH 1..3)");
+        case 3: launch_z_ns<FX, MAXT, MINB, 3, RPT>(a, nb, s); break;
+        case 4: launch_z_ns<FX, MAXT, MINB, 4, RPT>(a, nb, s); break;
+        default: throw Error(DOT_ERR_ARG, "z pass supports 3..4 ring slots (DOT_COCG_PREFETCH 1..2)");
     }
 }
 
 }  // namespace
 
-size_t zpass_smem(int nx, int TY, int NS) {
+size_t zpass_smem(int nx, int TY, int NS, int nz) {
     const size_t slotE = (size_t)(TY + 4) * nx;
     const size_t e = (size_t)NS * (2 * slotE + (nx % 2 == 0 ? (slotE + 1) / 2 : 0)) + 3 * (size_t)(TY + 2) * nx;
-    return e * sizeof(double2) + NS * 8 + 32 * kNumPartials * 8 + 128;
+    return e * sizeof(double2) + NS * 8 + 32 * kNumPartials * 8 + 8 * (size_t)nz + 128;
 }
 
 void launch_cocg_zpass(const PassArgs& a, int nb, cudaStream_t s) {
     const int maxt = a.tl.threads;
-    if (a.X) {
-        if (maxt <= 512) launch_z<true, 512, 1>(a, nb, s);
-        else launch_z<true, 1024, 1>(a, nb, s);
+    if (a.tl.zrows == 2) {
+        if (maxt > 512) throw Error(DOT_ERR_ARG, "z pass with 2 rows per thread supports <= 512 threads");
+        if (a.X) launch_z<true, 512, 1, 2>(a, nb, s);
+        else launch_z<false, 512, 1, 2>(a, nb, s);
         return;
     }
-    if (a.tl.minb >= 2) launch_z<false, 512, 2>(a, nb, s);
-    else if (maxt <= 512) launch_z<false, 512, 1>(a, nb, s);
-    else if (maxt <= 768) launch_z<false, 768, 1>(a, nb, s);
-    else launch_z<false, 1024, 1>(a, nb, s);
+    if (a.X) {
+        if (maxt <= 512) launch_z<true, 512, 1, 1>(a, nb, s);
+        else launch_z<true, 1024, 1, 1>(a, nb, s);
+        return;
+    }
+    if (a.tl.minb >= 2) launch_z<false, 512, 2, 1>(a, nb, s);
+    else if (maxt <= 512) launch_z<false, 512, 1, 1>(a, nb, s);
+    else if (maxt <= 768) launch_z<false, 768, 1, 1>(a, nb, s);
+    else launch_z<false, 1024, 1, 1>(a, nb, s);
 }
 
 }  // namespace dot

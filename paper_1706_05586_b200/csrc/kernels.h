@@ -13,6 +13,7 @@ struct CocgTiling {
     int kind = 1;         // 1: z-register pass (cocg_z.cu), 0: padded-ring pass (cocg.cu)
     int cluster = 1;      // thread-block cluster size along the tiles of one RHS (divides ntiles)
     int minb = 1;         // CTAs per SM the z pass is compiled for
+    int zrows = 1;        // z pass: slot rows per thread (1 or 2)
     int TY = 0, ntiles = 0, nslots = 0, threads = 512;
     int rpt = 0;          // x-rows covered by one sweep of the block (threads = roundup32(nx * rpt))
     size_t smem = 0;
@@ -67,7 +68,7 @@ void launch_clustered(K kernel, dim3 grid, int threads, size_t smem, cudaStream_
 }
 
 // z-register pass (cocg_z.cu)
-size_t zpass_smem(int nx, int TY, int NS);
+size_t zpass_smem(int nx, int TY, int NS, int nz);
 void launch_cocg_zpass(const PassArgs& a, int nb, cudaStream_t s);
 void launch_cocg_init(const PassArgs& a, int nb, cudaStream_t s);
 void launch_cocg_pass(const PassArgs& a, int nb, cudaStream_t s);

@@ -244,7 +244,8 @@ KNOBS = [dict(RING, DOT_COCG_THREADS="256"), dict(RING, DOT_COCG_THREADS="128"),
          # z-register pass: every thread-count option, ring depth, tile height and clusters
          dict(DOT_COCG_ZOPT="A"), dict(DOT_COCG_ZOPT="B"), dict(DOT_COCG_ZOPT="C"),
          dict(DOT_COCG_PREFETCH="1"), dict(DOT_COCG_PREFETCH="3"), dict(DOT_COCG_TY="3"), dict(DOT_COCG_TY="5"),
-         dict(DOT_COCG_TY="4", DOT_COCG_CLUSTER="2")]
+         dict(DOT_COCG_TY="4", DOT_COCG_CLUSTER="2"), dict(DOT_COCG_ZOPT="D"),
+         dict(DOT_COCG_ZOPT="D", DOT_COCG_TY="5"), dict(DOT_COCG_ZOPT="D", DOT_COCG_TY="3", DOT_COCG_PREFETCH="1")]
 
 
 @pytest.mark.parametrize("knobs", KNOBS)
