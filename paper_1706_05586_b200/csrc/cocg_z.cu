@@ -478,10 +478,18 @@ size_t zpass_smem(int nx, int TY, int NS, int nz) {
 
 void launch_cocg_zpass(const PassArgs& a, int nb, cudaStream_t s) {
     const int maxt = a.tl.threads;
-    if (a.tl.zrows == 2) {
-        if (maxt > 512) throw Error(DOT_ERR_ARG, "z pass with 2 rows per thread supports <= 512 threads");
-        if (a.X) launch_z<true, 512, 1, 2>(a, nb, s);
-        else launch_z<false, 512, 1, 2>(a, nb, s);
+    if (a.tl.zrows >= 2) {
+        if (maxt > 512) throw Error(DOT_ERR_ARG, "z pass with 2..4 rows per thread supports <= 512 threads");
+        if (a.tl.zrows == 2) {
+            if (a.X) launch_z<true, 512, 1, 2>(a, nb, s);
+            else launch_z<false, 512, 1, 2>(a, nb, s);
+        } else if (a.tl.zrows == 3) {
+            if (a.X) launch_z<true, 384, 1, 3>(a, nb, s);
+            else launch_z<false, 384, 1, 3>(a, nb, s);
+        } else {
+            if (a.X) launch_z<true, 256, 1, 4>(a, nb, s);
+            else launch_z<false, 256, 1, 4>(a, nb, s);
+        }
         return;
     }
     if (a.X) {
