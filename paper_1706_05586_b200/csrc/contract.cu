@@ -1,8 +1,16 @@
-// Jacobian contraction on FP64 tensor cores (DMMA):
+// Jacobian contraction on FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64 -- on
+// sm_100a the only FP64 tensor instruction; tcgen05.mma has no f64 kind):
 //   J[b][j][i][k] = - sum_s Lam[b][j][s] U[b][i][s] G[s][k]
 // (PAPER.md Eq. (Jacobian kth column), L966-972, with the sign of Eq. (2.8)).
 // GEMM view: rows m = 2*(j*ls + i) + c (c = re/im of the Hadamard product
-// Lam_j (.) U_i, formed in shared memory), K = |S|, N = n_p.
+// Lam_j (.) U_i, formed on the fly into shared memory), reduction over the
+// support K = |S|, columns n_p.
+//
+// CTA tile 128 rows (64 (j,i) pairs) x 8*NT columns (all parameters of a column
+// block, so each Hadamard product is formed once), k-tiles of 16 support points,
+// double-buffered in shared memory: the global loads of k-tile t+1 are issued
+// into registers before the DMMAs of tile t and land in the other buffer after
+// them -- one barrier per k-tile.  8 warps, warp w owns rows 16w .. 16w+15.
 #include "kernels.h"
 
 namespace dot {
@@ -10,10 +18,10 @@ namespace dot {
 namespace {
 
 constexpr int BM = 128;      // rows per CTA (64 complex pairs)
-constexpr int BN = 40;       // n_p columns per CTA (5 n8 fragments)
 constexpr int BK = 16;       // support points per k-tile
 constexpr int AS = BK + 4;   // padded row stride (doubles): conflict-free A fragments
-constexpr int GS = BN + 4;   // padded row stride of the G tile
+constexpr int THREADS = 256;
+constexpr int HPT = (BM / 2) * BK / THREADS;   // Hadamard products per thread per k-tile (4)
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -21,12 +29,18 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(256) contract_kernel(int K, int ld, int ls, int n_p,
-                                                       const double2* __restrict__ Lam, size_t lam_bs,
-                                                       const double2* __restrict__ U, size_t u_bs,
-                                                       const double* __restrict__ G, double2* J) {
-    __shared__ __align__(16) double As[BM * AS];
-    __shared__ __align__(16) double Gs[BK * GS];
+template <int NT>
+__global__ void __launch_bounds__(THREADS) contract_kernel(int K, int ld, int ls, int n_p,
+                                                           const double2* __restrict__ Lam, size_t lam_bs,
+                                                           const double2* __restrict__ U, size_t u_bs,
+                                                           const double* __restrict__ G, double2* J) {
+    constexpr int BN = 8 * NT;
+    constexpr int GS = BN + 4;                  // padded row stride of the G tile
+    constexpr int GPT = (BK * BN + THREADS - 1) / THREADS;
+    extern __shared__ __align__(16) double csm[];
+    // layout: A tiles [2][BM * AS], then G tiles [2][BK * GS]
+    auto Abuf = [&](int bb) { return csm + bb * (BM * AS); };
+    auto Gbuf = [&](int bb) { return csm + 2 * BM * AS + bb * (BK * GS); };
     const int b = blockIdx.z;
     const int npairs = ld * ls;
     const int pair0 = blockIdx.x * (BM / 2);
@@ -35,44 +49,85 @@ __global__ void __launch_bounds__(256) contract_kernel(int K, int ld, int ls, in
     const double2* Lb = Lam + (size_t)b * lam_bs;
     const double2* Ub = U + (size_t)b * u_bs;
 
-    double acc[2][5][2];
+    // per-thread Hadamard slots: element e = threadIdx.x + q*THREADS -> (lp, kk)
+    const double2* lrow[HPT];
+    const double2* urow[HPT];
+    bool pv[HPT];
+#pragma unroll
+    for (int q = 0; q < HPT; ++q) {
+        const int e = threadIdx.x + q * THREADS;
+        const int lp = e / BK;
+        const int pair = pair0 + lp;
+        pv[q] = pair < npairs;
+        const int j = pv[q] ? pair / ls : 0, i = pv[q] ? pair - j * ls : 0;
+        lrow[q] = Lb + (size_t)j * K + (e % BK);
+        urow[q] = Ub + (size_t)i * K + (e % BK);
+    }
+    double2 lv[HPT], uv[HPT];
+    double gv[GPT];
+    auto load = [&](int kt) {
+#pragma unroll
+        for (int q = 0; q < HPT; ++q) {
+            const int s = kt + ((threadIdx.x + q * THREADS) % BK);
+            const bool ok = pv[q] && s < K;
+            lv[q] = ok ? lrow[q][kt] : make_double2(0.0, 0.0);
+            uv[q] = ok ? urow[q][kt] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int q = 0; q < GPT; ++q) {
+            const int e = threadIdx.x + q * THREADS;
+            const int kk = e / BN, n = e % BN;
+            const int s = kt + kk, col = n0 + n;
+            gv[q] = (e < BK * BN && s < K && col < n_p) ? G[(size_t)s * n_p + col] : 0.0;
+        }
+    };
+    auto store = [&](int buf) {
+#pragma unroll
+        for (int q = 0; q < HPT; ++q) {
+            const int e = threadIdx.x + q * THREADS;
+            const int lp = e / BK, kk = e % BK;
+            const double2 v = cmul(lv[q], uv[q]);
+            double* A = Abuf(buf);
+            A[(2 * lp) * AS + kk] = v.x;
+            A[(2 * lp + 1) * AS + kk] = v.y;
+        }
+#pragma unroll
+        for (int q = 0; q < GPT; ++q) {
+            const int e = threadIdx.x + q * THREADS;
+            if (e < BK * BN) Gbuf(buf)[(e / BN) * GS + (e % BN)] = gv[q];
+        }
+    };
+
+    double acc[2][NT][2];
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 5; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        for (int ni = 0; ni < NT; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
+    load(0);
+    store(0);
+    __syncthreads();
+    int buf = 0;
     for (int kt = 0; kt < K; kt += BK) {
-        // Hadamard-formed A tile: 64 pairs x 16 points
-        for (int e = threadIdx.x; e < (BM / 2) * BK; e += blockDim.x) {
-            const int lp = e / BK, kk = e % BK;
-            const int pair = pair0 + lp, s = kt + kk;
-            double2 v = make_double2(0.0, 0.0);
-            if (pair < npairs && s < K) {
-                const int j = pair / ls, i = pair - j * ls;
-                v = cmul(Lb[(size_t)j * K + s], Ub[(size_t)i * K + s]);
-            }
-            As[(2 * lp) * AS + kk] = v.x;
-            As[(2 * lp + 1) * AS + kk] = v.y;
-        }
-        for (int e = threadIdx.x; e < BK * BN; e += blockDim.x) {
-            const int kk = e / BN, n = e % BN;
-            const int s = kt + kk, col = n0 + n;
-            Gs[kk * GS + n] = (s < K && col < n_p) ? G[(size_t)s * n_p + col] : 0.0;
-        }
-        __syncthreads();
+        const bool more = kt + BK < K;
+        if (more) load(kt + BK);                 // global loads in flight during the DMMAs
+        const double* A = Abuf(buf);
+        const double* Bt = Gbuf(buf);
 #pragma unroll
         for (int k4 = 0; k4 < BK; k4 += 4) {
-            double af[2], bf[5];
+            double af[2], bf[NT];
 #pragma unroll
-            for (int mi = 0; mi < 2; ++mi) af[mi] = As[(warp * 16 + mi * 8 + (lane >> 2)) * AS + k4 + (lane & 3)];
+            for (int mi = 0; mi < 2; ++mi) af[mi] = A[(warp * 16 + mi * 8 + (lane >> 2)) * AS + k4 + (lane & 3)];
 #pragma unroll
-            for (int ni = 0; ni < 5; ++ni) bf[ni] = Gs[(k4 + (lane & 3)) * GS + ni * 8 + (lane >> 2)];
+            for (int ni = 0; ni < NT; ++ni) bf[ni] = Bt[(k4 + (lane & 3)) * GS + ni * 8 + (lane >> 2)];
 #pragma unroll
             for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-                for (int ni = 0; ni < 5; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+                for (int ni = 0; ni < NT; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
         }
+        if (more) store(buf ^ 1);
         __syncthreads();
+        buf ^= 1;
     }
     // epilogue: row m -> (pair, c); J[b][pair][n] complex, negated (Eq. (2.8))
     double* Jd = reinterpret_cast<double*>(J);
@@ -82,7 +137,7 @@ __global__ void __launch_bounds__(256) contract_kernel(int K, int ld, int ls, in
         const int pair = pair0 + (m >> 1), c = m & 1;
         if (pair >= npairs) continue;
 #pragma unroll
-        for (int ni = 0; ni < 5; ++ni) {
+        for (int ni = 0; ni < NT; ++ni) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int col = n0 + ni * 8 + 2 * (lane & 3) + h;
@@ -90,6 +145,21 @@ __global__ void __launch_bounds__(256) contract_kernel(int K, int ld, int ls, in
             }
         }
     }
+}
+
+template <int NT>
+void launch_nt(int nb, int K, int ld, int ls, int n_p, const double2* Lam, size_t lam_bstride, const double2* U,
+               size_t u_bstride, const double* G, double2* J, cudaStream_t s) {
+    const int npairs = ld * ls;
+    dim3 grid((npairs + BM / 2 - 1) / (BM / 2), (n_p + 8 * NT - 1) / (8 * NT), nb);
+    const size_t smem = (size_t)(2 * BM * AS + 2 * BK * (8 * NT + 4)) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        DOT_CUDA_TRY(cudaFuncSetAttribute(contract_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    contract_kernel<NT><<<grid, THREADS, smem, s>>>(K, ld, ls, n_p, Lam, lam_bstride, U, u_bstride, G, J);
+    DOT_CUDA_TRY(cudaGetLastError());
 }
 
 }  // namespace
@@ -102,9 +172,10 @@ void launch_contract(int nb, int K, int ld, int ls, int n_p, const double2* Lam,
         DOT_CUDA_TRY(cudaMemsetAsync(J, 0, (size_t)nb * npairs * n_p * sizeof(double2), s));
         return;
     }
-    dim3 grid((npairs + BM / 2 - 1) / (BM / 2), (n_p + BN - 1) / BN, nb);
-    contract_kernel<<<grid, 256, 0, s>>>(K, ld, ls, n_p, Lam, lam_bstride, U, u_bstride, G, J);
-    DOT_CUDA_TRY(cudaGetLastError());
+    // all parameters of a column block in one CTA (one Hadamard formation per pair)
+    if (n_p <= 24) launch_nt<3>(nb, K, ld, ls, n_p, Lam, lam_bstride, U, u_bstride, G, J, s);
+    else if (n_p <= 40) launch_nt<5>(nb, K, ld, ls, n_p, Lam, lam_bstride, U, u_bstride, G, J, s);
+    else launch_nt<10>(nb, K, ld, ls, n_p, Lam, lam_bstride, U, u_bstride, G, J, s);
 }
 
 }  // namespace dot
