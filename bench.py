@@ -311,10 +311,12 @@ def main():
     peak, peak_src = measured_peaks()
     gbs = (st["pass_bytes"] - s0["pass_bytes"]) / max(st["pass_ms"] - s0["pass_ms"], 1e-9) / 1e6
     traffic = ncu_traffic()
-    roof = {"bound": "hbm", "kernel": "cocg_pass_kernel", "achieved": gbs, "peak": peak, "unit": "GB/s",
+    roof = {"bound": "hbm", "kernel": "cocg_zpass_kernel", "achieved": gbs, "peak": peak, "unit": "GB/s",
             "frac": gbs / peak, "peak_source": peak_src,
-            "algorithmic_bytes": "64 B per grid point per COCG iteration per RHS (read r,p; write r,p)",
-            "traffic": traffic["bytes_per_point_iter"] if traffic else None,
+            "algorithmic_bytes": "64 B per grid point per COCG iteration per RHS (read r_k, p_k-1; write r_k+1, p_k)",
+            "traffic": traffic["dram_bytes"] if traffic else None,
+            "traffic_algorithmic": traffic["algorithmic_bytes_if_all_active"] if traffic else None,
+            "traffic_ratio": traffic["ratio"] if traffic else None,
             "traffic_note": traffic["note"] if traffic else "no ncu --set full capture committed yet"}
     jf = st["contract_flops"] / max(st["contract_ms"], 1e-9) / 1e9
     fpk, fsrc = fp64_peak()
