@@ -1,0 +1,112 @@
+"""Parity at BASELINE.json's full bench size (configs[2], `full64`: 64^3, 256 sources x
+256 detectors x 3 frequencies, 80 parameters) in the launch configuration bench.py
+times (dot_jacobian(I, I): all 1536 forward + adjoint RHS iterated in one batch).
+
+The oracle's sparse LU at 64^3 takes minutes, so these tests check what the oracle
+can compute one by one and properties that hold at any size (task statement (3)):
+  * the true residual ||b - A x|| / ||b|| of dense solves, with A assembled by the
+    oracle (Eq. (2.1); reading R12: attainable ~4e-16 at tol 1e-17);
+  * the sampled solutions the batched solve keeps equal the dense solutions there;
+  * reciprocity c_d^T A^-1 b_s = (A^-T c_d)^T b_s over all 256 x 256 x 3 pairs --
+    forward solves against adjoint solves (A complex symmetric, north_star pin);
+  * Jacobian entries (Eq. (Jacobian kth column), L966-972) against the direct sum
+    over the dense fields and the oracle's dA/dp weights, 1e-7 relative Frobenius.
+"""
+import numpy as np
+import pytest
+
+from oracle import absorption, jacobian_weights, make_grid
+from synth import config_by_name, make_workload
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def full():
+    from paper_1706_05586_b200 import build
+    build.build()
+    import paper_1706_05586_b200 as dot
+    cfg = config_by_name("full64")
+    wl = make_workload(cfg)
+    g = dot.DOTProblem.from_config(cfg, wl.src_nodes, wl.det_nodes)
+    g.set_params(wl.p)
+    J = g.jacobian(None, None)                       # the bench's batch: 1536 RHS in one launch sequence
+    grid = make_grid(cfg.n, cfg.L)
+    return dict(dot=dot, cfg=cfg, wl=wl, g=g, J=J, grid=grid)
+
+
+def _operator(full, f):
+    from oracle import assemble
+    cfg, wl, grid = full["cfg"], full["wl"], full["grid"]
+    mu = absorption(wl.p, grid, cfg)
+    return assemble(grid, cfg.D, mu, 2 * np.pi * cfg.freqs_hz[f], cfg.nu).tocsr()
+
+
+def test_full64_dense_solves_true_residual_and_sampled_agree(full):
+    g, cfg, wl, grid = full["g"], full["cfg"], full["wl"], full["grid"]
+    N = grid.N
+    samp = g.samples()
+    X = g.solve_sampled(0)                           # cached fields of the batched solve
+    scale = grid.theta[wl.src_nodes] / grid.cell_volume
+    for f in (0, 2):
+        A = _operator(full, f)
+        cols = [0, 137]
+        b = np.zeros((len(cols), N), complex)
+        for r, c in enumerate(cols):
+            b[r, wl.src_nodes[c]] = scale[c]
+        x, iters = g.solve(b, f)
+        for r, c in enumerate(cols):
+            res = np.linalg.norm(b[r] - A @ x[r]) / np.linalg.norm(b[r])
+            assert res < 1e-14, (f, c, res)
+            xs = X[f, c]
+            assert np.abs(xs - x[r][samp]).max() <= 1e-10 * np.abs(x[r][samp]).max()
+            # detectors: the far-field values the misfit is made of
+            xd, xdr = X[f, c][np.searchsorted(samp, wl.det_nodes)], x[r][wl.det_nodes]
+            assert np.linalg.norm(xd - xdr) <= 1e-9 * np.linalg.norm(xdr)
+
+
+def test_full64_reciprocity_all_pairs(full):
+    g, cfg, wl, grid = full["g"], full["cfg"], full["wl"], full["grid"]
+    samp = g.samples()
+    Xs = g.solve_sampled(0)                          # [f][s][P] forward fields
+    Xd = g.solve_sampled(1)                          # [f][d][P] adjoint fields
+    di = np.searchsorted(samp, wl.det_nodes)
+    si = np.searchsorted(samp, wl.src_nodes)
+    scale = grid.theta[wl.src_nodes] / grid.cell_volume
+    for f in range(cfg.n_freq):
+        M_fwd = Xs[f][:, di].T                       # [d][s] = c_d^T A^-1 b_s
+        M_adj = Xd[f][:, si] * scale[None, :]        # [d][s] = (A^-T c_d)^T b_s
+        rel = np.linalg.norm(M_fwd - M_adj) / np.linalg.norm(M_fwd)
+        assert rel < 1e-9, (f, rel)
+
+
+def test_full64_jacobian_entries_against_dense_fields(full):
+    g, cfg, wl, grid = full["g"], full["cfg"], full["wl"], full["grid"]
+    N = grid.N
+    Jg = full["J"]                                   # [f][ld][ls][n_p] = (I (x) I) J
+    Gfull = jacobian_weights(wl.p, grid, cfg)        # oracle dA/dp diagonal, [N][n_p]
+    scale = grid.theta[wl.src_nodes] / grid.cell_volume
+    src_cols, det_cols = [3, 200], [17, 250]
+    for f in (1,):
+        b = np.zeros((len(src_cols), N), complex)
+        for r, c in enumerate(src_cols):
+            b[r, wl.src_nodes[c]] = scale[c]
+        z, _ = g.solve(b, f)
+        c = np.zeros((len(det_cols), N), complex)
+        for r, d in enumerate(det_cols):
+            c[r, wl.det_nodes[d]] = 1.0
+        y, _ = g.solve(c, f)                          # A^T = A
+        S = np.nonzero(np.abs(Gfull).sum(1) > 0)[0]      # support of dA/dp (L972)
+        ref = -np.einsum("jx,xk,ix->jik", y[:, S], Gfull[S], z[:, S])
+        got = Jg[f][np.ix_(det_cols, src_cols)]
+        assert np.linalg.norm(got - ref) <= 1e-7 * np.linalg.norm(ref)
+
+
+def test_full64_sketched_jacobian_is_combination_of_full(full):
+    """(W^T (x) V^T) J from the cached fields equals the W, V combination of the full
+    J, at the bench's sketch W, V (Rademacher 256 x 12)."""
+    g, wl = full["g"], full["wl"]
+    Jf = full["J"]
+    Js = g.jacobian(wl.W, wl.V)
+    ref = np.einsum("sl,dm,fdsk->fmlk", wl.W, wl.V, Jf)
+    assert np.linalg.norm(Js - ref) <= 1e-10 * np.linalg.norm(ref)
