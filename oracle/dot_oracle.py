@@ -20,6 +20,8 @@ Pins (tests/test_oracle_*.py, all ``-m "not gpu"``):
   jacobian      central finite differences of the sketched residual
   optimize      Lemma 3.2 optimality certificates, dominance over random feasible
                 candidates, angular brute force, Table 1 SVD sizes (golden)
+  subspace      converges to the exact Theorem 3.6/3.7 direction; one step equals the
+                brute-force best direction in span(P X0) (Rayleigh-Ritz); orthogonality
 No function here is "parity unpinned".
 """
 from __future__ import annotations
@@ -36,7 +38,7 @@ __all__ = [
     "source_matrix", "detector_matrix", "Problem", "make_problem", "simulate_data",
     "measurements", "sketched_residual", "misfit", "jacobian", "jacobian_from_fields",
     "frob_objective", "remove_sources", "remove_detectors", "add_sources", "add_detectors",
-    "optimize_directions", "complement_basis",
+    "optimize_directions", "complement_basis", "subspace_add_direction", "optimize_directions_subspace",
 ]
 
 
@@ -438,4 +440,80 @@ def optimize_directions(prob: Problem, p, W, V, s, trace=None):
         V = np.concatenate([V, np.sqrt(nd) * q], axis=1)
         if trace is not None:
             trace.append(("add_detector", shape, frob_objective(jac(W, V))))
+    return W, V
+
+
+# ------------------------ optimized directions by subspace iteration (reading R16)
+def _orth(M):
+    """Orthonormal basis of span(M) (reduced QR)."""
+    Q, _ = np.linalg.qr(M)
+    return Q
+
+
+def _sign_fix(q):
+    """Sign convention shared with the GPU path: the largest-magnitude entry is positive."""
+    i = int(np.argmax(np.abs(q)))
+    return q if q[i] >= 0 else -q
+
+
+def subspace_add_direction(Xr, M, X0, iters):
+    """Matrix-free form of Theorems 3.6 / 3.7 by subspace iteration
+    (BASELINE.json configs[3] "5 subspace iterations maximizing ||V^T J W||_F";
+    reading R16).  Xr: (n, m) real unfolding [Re, Im] of V^T-combined (or W-combined)
+    Jacobian slices, M: (n, l) current directions, X0: (n, p) starting block (caller's
+    random draws).  With P = I - Q_M Q_M^T and K = P Xr Xr^T P:
+        Q_0 = orth(P X0);  Y_t = K Q_{t-1},  Q_t = orth(Y_t)  (t = 1 .. iters-1);
+        Y_iters = K Q_{iters-1};  H = Q^T Y (Rayleigh-Ritz);  q = Q e_max(H).
+    As iters grows, q -> V_c phi_1 of Theorem 3.6 (top left singular vector of
+    V_c^T [J^_1 .. J^_ls]).  Returns the unit vector q (sign: largest entry > 0)."""
+    n = Xr.shape[0]
+    QM = _orth(M)
+    P = np.eye(n) - QM @ QM.T
+    K = P @ Xr @ Xr.T @ P
+    Q = _orth(P @ X0)
+    Y = K @ Q
+    for _ in range(iters - 1):
+        Q = _orth(Y)
+        Y = K @ Q
+    H = Q.T @ Y
+    H = 0.5 * (H + H.T)
+    w, E = np.linalg.eigh(H)
+    q = Q @ E[:, np.argmax(w)]
+    q = P @ q
+    return _sign_fix(q / np.linalg.norm(q))
+
+
+def optimize_directions_subspace(prob: Problem, p, W, V, s, iters, X0_src, X0_det):
+    """Two-phase replacement of s directions where the add steps
+    use subspace_add_direction instead of the exact SVD (reading R16); the remove
+    steps are Theorems 3.5 / 3.4 as in optimize_directions.  The oracle builds the
+    explicit Jacobian slices from all-source / all-detector LU solves; the GPU path
+    applies K matrix-free with 2 n_freq solves per block vector per iteration."""
+    ns, nd = W.shape[0], V.shape[0]
+    G = jacobian_weights(p, prob.grid, prob.cfg)
+    U_all, L_all = [], []
+    for f in range(len(prob.omegas)):
+        lu = prob.factor(p, f)
+        U_all.append(prob.solve(lu, prob.B))
+        L_all.append(prob.solve(lu, prob.C, trans="T"))
+
+    def jac(Wm, Vm):
+        return np.stack([jacobian_from_fields(U_all[f] @ Wm, L_all[f] @ Vm, G)
+                         for f in range(len(prob.omegas))])
+
+    W, V = np.array(W, dtype=np.float64), np.array(V, dtype=np.float64)
+    for _ in range(s):                         # phase one: remove (exact, Theorems 3.5, 3.4)
+        Gam, _ = remove_sources(jac(W, V), 1)
+        W = W @ Gam
+        Gam, _ = remove_detectors(jac(W, V), 1)
+        V = V @ Gam
+    for _ in range(s):                         # phase two: add by subspace iteration
+        J_IV = jac(np.eye(ns), V)               # (nf, ld, ns, n_p)
+        Xr = _real_rows(np.transpose(J_IV, (2, 0, 1, 3)).reshape(ns, -1))
+        q = subspace_add_direction(Xr, W, X0_src, iters)
+        W = np.concatenate([W, np.sqrt(ns) * q[:, None]], axis=1)
+        J_WI = jac(W, np.eye(nd))               # (nf, nd, ls, n_p)
+        Xr = _real_rows(np.transpose(J_WI, (1, 0, 2, 3)).reshape(nd, -1))
+        q = subspace_add_direction(Xr, V, X0_det, iters)
+        V = np.concatenate([V, np.sqrt(nd) * q[:, None]], axis=1)
     return W, V

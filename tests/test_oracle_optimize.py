@@ -137,3 +137,81 @@ def test_optimize_directions_end_to_end():
     # the kept random subspace is inside the original span
     P = W @ np.linalg.pinv(W)
     assert np.abs(P @ Wn[:, :-1] - Wn[:, :-1]).max() < 1e-10
+
+
+# ------------------------------------------------ subspace iteration (reading R16)
+from oracle import optimize_directions_subspace, subspace_add_direction  # noqa: E402
+from oracle.dot_oracle import _real_rows  # noqa: E402
+
+
+def _xr_detectors(Jf, W):
+    """Real unfolding [Re, Im] of (W^T (x) I) J as the n_d x (2 nf ls n_p) matrix of Theorem 3.6."""
+    nf, nd = Jf.shape[0], Jf.shape[1]
+    J_WI = _sk(Jf, W, np.eye(nd))
+    return _real_rows(np.transpose(J_WI, (1, 0, 2, 3)).reshape(nd, -1))
+
+
+@pytest.mark.parametrize("trial", range(5))
+def test_subspace_iteration_converges_to_theorem_3_6(trial):
+    rng = np.random.default_rng(100 + trial)
+    nf, nd, ns, n_p, ls, ld = 2, 9, 7, 4, 3, 3
+    Jf = _jfull(rng, nf, nd, ns, n_p)
+    W, V = _rand_orth(rng, ns, ls), _rand_orth(rng, nd, ld)
+    q_exact, _, _ = add_detectors(_sk(Jf, W, np.eye(nd)), V, 1)
+    q = subspace_add_direction(_xr_detectors(Jf, W), V, rng.standard_normal((nd, 2)), 400)
+    assert abs(float(q @ q_exact[:, 0])) > 1 - 1e-10
+    assert np.linalg.norm(q) == pytest.approx(1.0)
+    assert np.abs(V.T @ q).max() < 1e-12
+    assert q[np.argmax(np.abs(q))] > 0
+
+
+def test_subspace_single_step_is_best_direction_in_start_span():
+    """iters = 1 is Rayleigh-Ritz on span(P X0): its direction maximises ||Xr^T q|| over
+    that 2-D span -- checked against a brute-force angular sweep."""
+    rng = np.random.default_rng(7)
+    nf, nd, ns, n_p, ls, ld = 1, 8, 6, 3, 2, 3
+    Jf = _jfull(rng, nf, nd, ns, n_p)
+    W, V = _rand_orth(rng, ns, ls), _rand_orth(rng, nd, ld)
+    Xr = _xr_detectors(Jf, W)
+    X0 = rng.standard_normal((nd, 2))
+    q = subspace_add_direction(Xr, V, X0, 1)
+    Pm = np.eye(nd) - V @ V.T
+    B, _ = np.linalg.qr(Pm @ X0)
+    th = np.linspace(0, np.pi, 20001)
+    cand = B @ np.stack([np.cos(th), np.sin(th)])
+    vals = np.sum((Xr.T @ cand) ** 2, axis=0)
+    best = float(np.sum((Xr.T @ q) ** 2))
+    assert best >= vals.max() * (1 - 1e-12)
+    assert best <= vals.max() * (1 + 1e-6)
+
+
+def test_subspace_objective_grows_with_iterations():
+    rng = np.random.default_rng(11)
+    nf, nd, ns, n_p, ls, ld = 2, 12, 5, 3, 2, 4
+    Jf = _jfull(rng, nf, nd, ns, n_p)
+    W, V = _rand_orth(rng, ns, ls), _rand_orth(rng, nd, ld)
+    Xr = _xr_detectors(Jf, W)
+    X0 = rng.standard_normal((nd, 2))
+    q_exact, _, _ = add_detectors(_sk(Jf, W, np.eye(nd)), V, 1)
+    top = float(np.sum((Xr.T @ q_exact[:, 0]) ** 2))
+    vals = [float(np.sum((Xr.T @ subspace_add_direction(Xr, V, X0, it)) ** 2)) for it in (1, 2, 5, 50)]
+    assert all(v <= top * (1 + 1e-12) for v in vals)
+    assert vals[-1] == pytest.approx(top, rel=1e-9)
+    assert vals[0] <= vals[2] + 1e-12 * top
+
+
+def test_optimize_directions_subspace_matches_exact_when_converged():
+    cfg = small_config(n=(7, 7, 6), src=(3, 2), det=(3, 2), eps=0.4)
+    prob, wl = small_problem(cfg, with_data=False)
+    rng = np.random.default_rng(3)
+    W, V = np.sign(rng.standard_normal((6, 3))), np.sign(rng.standard_normal((6, 3)))
+    X0s, X0d = rng.standard_normal((6, 2)), rng.standard_normal((6, 2))
+    We, Ve = optimize_directions(prob, wl.p, W, V, 1)
+    Ws, Vs = optimize_directions_subspace(prob, wl.p, W, V, 1, 300, X0s, X0d)
+    # kept columns identical (same remove steps); new columns equal up to sign
+    assert np.abs(Ws[:, :-1] - We[:, :-1]).max() < 1e-9
+    assert abs(float(Ws[:, -1] @ We[:, -1])) / 6 > 1 - 1e-8
+    assert abs(float(Vs[:, -1] @ Ve[:, -1])) / 6 > 1 - 1e-8
+    o5 = frob_objective(jacobian(prob, wl.p, *optimize_directions_subspace(prob, wl.p, W, V, 1, 5, X0s, X0d)))
+    oe = frob_objective(jacobian(prob, wl.p, We, Ve))
+    assert o5 <= oe * (1 + 1e-9)
