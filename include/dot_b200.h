@@ -157,6 +157,23 @@ int dot_optimize_directions(dot_problem* P, int32_t k, const double* W, int32_t 
                             const double* V, int32_t ld, int where,
                             double* W_out, double* V_out, double* objective_out);
 
+/* optimize_directions by subspace iteration (reading R16; BASELINE.json
+ * configs[3] "optimized ... found by 5 subspace iterations maximizing ||V^T J W||_F"):
+ * same two-phase replacement as dot_optimize_directions, but the add steps
+ * (Theorems 3.7, 3.6) find the new direction by `iters` steps of
+ * subspace iteration with a `block`-vector block on P Xr Xr^T P, applied matrix-free
+ * (2 n_freq solves per block vector per step) -- no full-data solves.  The remove
+ * steps (Theorems 3.5, 3.4) use the sketched Jacobian of the current W, V
+ * (ls + ld solves per frequency, combined without new solves afterwards).
+ * X0_src [n_src][k*block], X0_det [n_det][k*block]: starting blocks (the caller's
+ * random draws); add step t starts from columns t*block .. (t+1)*block - 1.  New columns: unit direction with
+ * its largest-magnitude entry positive, scaled to length sqrt(n).  Errors as
+ * dot_optimize_directions; DOT_ERR_ARG if block exceeds the complement dimension. */
+int dot_optimize_directions_subspace(dot_problem* P, int32_t k, int32_t iters, int32_t block, const double* W,
+                                     int32_t ls, const double* V, int32_t ld, const double* X0_src,
+                                     const double* X0_det, int where, double* W_out, double* V_out,
+                                     double* objective_out);
+
 /* ---- component calls (same kernels; used by the parity tests) ---- */
 
 /* mu(x, p) of the last set_params: mu_out [N] real. */

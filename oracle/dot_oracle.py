@@ -486,7 +486,9 @@ def subspace_add_direction(Xr, M, X0, iters):
 def optimize_directions_subspace(prob: Problem, p, W, V, s, iters, X0_src, X0_det):
     """Two-phase replacement of s directions where the add steps
     use subspace_add_direction instead of the exact SVD (reading R16); the remove
-    steps are Theorems 3.5 / 3.4 as in optimize_directions.  The oracle builds the
+    steps are Theorems 3.5 / 3.4 as in optimize_directions.  X0_src (n_s, s*blk),
+    X0_det (n_d, s*blk): add step t starts from columns t*blk .. (t+1)*blk - 1 (a block
+    reused after its own Ritz vector was added would be rank deficient).  The oracle builds the
     explicit Jacobian slices from all-source / all-detector LU solves; the GPU path
     applies K matrix-free with 2 n_freq solves per block vector per iteration."""
     ns, nd = W.shape[0], V.shape[0]
@@ -507,13 +509,14 @@ def optimize_directions_subspace(prob: Problem, p, W, V, s, iters, X0_src, X0_de
         W = W @ Gam
         Gam, _ = remove_detectors(jac(W, V), 1)
         V = V @ Gam
-    for _ in range(s):                         # phase two: add by subspace iteration
+    blk = X0_src.shape[1] // s
+    for t in range(s):                         # phase two: add by subspace iteration
         J_IV = jac(np.eye(ns), V)               # (nf, ld, ns, n_p)
         Xr = _real_rows(np.transpose(J_IV, (2, 0, 1, 3)).reshape(ns, -1))
-        q = subspace_add_direction(Xr, W, X0_src, iters)
+        q = subspace_add_direction(Xr, W, X0_src[:, t * blk:(t + 1) * blk], iters)
         W = np.concatenate([W, np.sqrt(ns) * q[:, None]], axis=1)
         J_WI = jac(W, np.eye(nd))               # (nf, nd, ls, n_p)
         Xr = _real_rows(np.transpose(J_WI, (1, 0, 2, 3)).reshape(nd, -1))
-        q = subspace_add_direction(Xr, V, X0_det, iters)
+        q = subspace_add_direction(Xr, V, X0_det[:, t * blk:(t + 1) * blk], iters)
         V = np.concatenate([V, np.sqrt(nd) * q[:, None]], axis=1)
     return W, V

@@ -187,6 +187,23 @@ class DOTProblem:
                                                       C.byref(obj)))
         return Wo, Vo, obj.value
 
+    def optimize_directions_subspace(self, k, W, V, X0_src, X0_det, iters=5):
+        """Replace k random simultaneous sources/detectors by optimized ones found by
+        `iters` subspace-iteration steps, matrix-free.  X0_src [n_src][k*block],
+        X0_det [n_det][k*block]: add step t starts from block t.
+        Returns (W_hat, V_hat, objective)."""
+        a = _Args(_where_of(W, V))
+        if k < 1 or X0_src.shape[1] % k or X0_det.shape[1] != X0_src.shape[1]:
+            raise ValueError("X0_src, X0_det need k*block columns")
+        blk = int(X0_src.shape[1]) // k
+        Wo, wp = a.out(tuple(W.shape), np.float64)
+        Vo, vp = a.out(tuple(V.shape), np.float64)
+        obj = C.c_double()
+        self._check(self._lib.dot_optimize_directions_subspace(
+            self._h, int(k), int(iters), blk, a.ptr(W, np.float64), int(W.shape[1]), a.ptr(V, np.float64),
+            int(V.shape[1]), a.ptr(X0_src, np.float64), a.ptr(X0_det, np.float64), a.where, wp, vp, C.byref(obj)))
+        return Wo, Vo, obj.value
+
     # ------------------------------------------------------------ components
     def absorption(self):
         a = _Args(DOT_HOST)

@@ -61,6 +61,9 @@ SIGNATURES = {
     "dot_jacobian": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int, C.c_void_p]),
     "dot_optimize_directions": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
                                           C.c_int, C.c_void_p, C.c_void_p, dp]),
+    "dot_optimize_directions_subspace": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                                   C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                                   C.c_int, C.c_void_p, C.c_void_p, dp]),
     "dot_absorption": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     "dot_support": (C.c_int, [C.c_void_p, i32p, C.c_void_p, C.c_void_p, C.c_int]),
     "dot_apply": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int]),

@@ -52,7 +52,7 @@ struct dot_problem {
     std::vector<double> params;
     // support S and sample set P = S u detectors
     int K = 0, nP = 0;
-    DBuf<int32_t> d_S, d_P, d_S_slot, d_det_slot, d_off;
+    DBuf<int32_t> d_S, d_P, d_S_slot, d_det_slot, d_src_slot, d_off;
     DBuf<double> d_G;
     DBuf<double2> d_Dt;               // data, [n_freq][n_src][n_det]
     FieldCache cache[2];              // 0: sources, 1: detectors
@@ -485,7 +485,7 @@ int dot_bind_workspace(dot_problem* P, void* ptr, size_t bytes) {
     if ((reinterpret_cast<uintptr_t>(ptr) & 255) != 0) throw Error(DOT_ERR_ARG, "workspace must be 256-byte aligned");
     // drop everything allocated from the old workspace
     invalidate_caches(P);
-    P->d_S.reset(); P->d_P.reset(); P->d_S_slot.reset(); P->d_det_slot.reset(); P->d_off.reset(); P->d_G.reset();
+    P->d_S.reset(); P->d_P.reset(); P->d_S_slot.reset(); P->d_det_slot.reset(); P->d_src_slot.reset(); P->d_off.reset(); P->d_G.reset();
     P->d_Dt.reset(); P->d_src.reset(); P->d_det.reset(); P->d_src_scale.reset(); P->d_det_scale.reset();
     P->d_omega_nu.reset(); P->d_mu.reset(); P->d_params.reset(); P->d_flagS.reset(); P->d_flagP.reset();
     P->d_posS.reset(); P->d_posP.reset(); P->d_scan_tmp.reset(); P->d_tot.reset(); P->d_count.reset();
@@ -571,17 +571,19 @@ int dot_set_params(dot_problem* P, const double* p, int where) {
     sync(P);
     P->K = tot[0];
     P->nP = tot[1];
-    P->d_S.reset(); P->d_P.reset(); P->d_S_slot.reset(); P->d_det_slot.reset(); P->d_off.reset(); P->d_G.reset();
+    P->d_S.reset(); P->d_P.reset(); P->d_S_slot.reset(); P->d_det_slot.reset(); P->d_src_slot.reset(); P->d_off.reset(); P->d_G.reset();
     P->d_S = DBuf<int32_t>(P->arena, std::max(P->K, 1));
     P->d_P = DBuf<int32_t>(P->arena, std::max(P->nP, 1));
     P->d_S_slot = DBuf<int32_t>(P->arena, std::max(P->K, 1));
     P->d_det_slot = DBuf<int32_t>(P->arena, P->n_det);
+    P->d_src_slot = DBuf<int32_t>(P->arena, P->n_src);
     P->d_off = DBuf<int32_t>(P->arena, (size_t)P->nz * P->tl.ntiles + 1);
     P->d_G = DBuf<double>(P->arena, std::max<size_t>((size_t)P->K * P->n_p, 1));
     launch_compact(P->d_flagS.get(), P->d_posS.get(), N, P->d_S.get(), s);
     launch_compact(P->d_flagP.get(), P->d_posP.get(), N, P->d_P.get(), s);
     launch_gather_rank(P->d_posP.get(), P->d_S.get(), P->K, P->d_S_slot.get(), s);
     launch_gather_rank(P->d_posP.get(), P->d_det.get(), P->n_det, P->d_det_slot.get(), s);
+    launch_gather_rank(P->d_posP.get(), P->d_src.get(), P->n_src, P->d_src_slot.get(), s);
     launch_pals_grad(P->pc, P->d_params.get(), P->d_S.get(), P->K, P->d_G.get(), s);
     launch_sample_offsets(P->d_P.get(), P->nP, P->nx, P->ny, P->nz, P->tl.TY, P->tl.ntiles, P->d_off.get(), s);
     P->stats.kernel_launches += 6;
@@ -697,6 +699,76 @@ int dot_optimize_directions(dot_problem* P, int32_t k, const double* W, int32_t 
     OptContext oc{P->arena, P->stream, P->n_freq, P->n_src, P->n_det, P->n_p, P->K, P->nP,
                   XU, XL, P->d_S_slot.get(), P->d_G.get(), &P->stats.kernel_launches};
     double obj = optimize_two_phase(oc, k, hW, ls, hV, ld);
+    if (objective_out) *objective_out = obj;
+    if (where == DOT_HOST) {
+        std::memcpy(W_out, hW.data(), hW.size() * sizeof(double));
+        std::memcpy(V_out, hV.data(), hV.size() * sizeof(double));
+    } else {
+        DOT_CUDA_TRY(cudaMemcpyAsync(W_out, hW.data(), hW.size() * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+        DOT_CUDA_TRY(cudaMemcpyAsync(V_out, hV.data(), hV.size() * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+        sync(P);
+    }
+    DOT_API_END(P)
+}
+
+int dot_optimize_directions_subspace(dot_problem* P, int32_t k, int32_t iters, int32_t block, const double* W,
+                                     int32_t ls, const double* V, int32_t ld, const double* X0_src,
+                                     const double* X0_det, int where, double* W_out, double* V_out,
+                                     double* objective_out) {
+    DOT_API_BEGIN
+    if (!P || !W || !V || !X0_src || !X0_det || !W_out || !V_out) throw Error(DOT_ERR_ARG, "null argument");
+    require_params(P);
+    if (k < 0 || k >= ls || k >= ld) throw Error(DOT_ERR_ARG, "need 0 <= k < min(ls, ld)");
+    if (iters < 1 || block < 1) throw Error(DOT_ERR_ARG, "need iters >= 1 and block >= 1");
+    if (block > P->n_src - ls + k || block > P->n_det - ld + k)
+        throw Error(DOT_ERR_ARG, "block larger than the complement of the kept directions");
+    std::vector<double> hW = host_copy(P, W, (size_t)P->n_src * ls, where);
+    std::vector<double> hV = host_copy(P, V, (size_t)P->n_det * ld, where);
+    std::vector<double> hXs = host_copy(P, X0_src, (size_t)P->n_src * block * std::max(k, 1), where);
+    std::vector<double> hXd = host_copy(P, X0_det, (size_t)P->n_det * block * std::max(k, 1), where);
+    const int nf = P->n_freq, K = P->K, nP = P->nP;
+    cudaStream_t s = P->stream;
+    SubspaceOps ops;
+    ops.fields = [&](int side, const std::vector<double>& coeff, int ncols, double2* out) {
+        DBuf<double> dc = to_device(P, coeff.data(), coeff.size(), DOT_HOST);
+        DBuf<double2> XP(P->arena, std::max<size_t>((size_t)nf * ncols * nP, 1));
+        solve_rhs(P, side, dc.get(), ncols, nf * ncols, nullptr, nullptr, XP.get(), nullptr);
+        launch_gather_cols(nf, ncols, K, XP.get(), (size_t)ncols * nP, nP, P->d_S_slot.get(), out, (size_t)ncols * K,
+                           K, s);
+        P->stats.kernel_launches++;
+        sync(P);
+    };
+    ops.solve_support = [&](const double2* w, int nvec, int side, double2* out) {
+        const int nr = nf * nvec;
+        DBuf<double2> R(P->arena, (size_t)nr * P->N);
+        DOT_CUDA_TRY(cudaMemsetAsync(R.get(), 0, (size_t)nr * P->N * sizeof(double2), s));
+        launch_scatter_support(R.get(), P->N, nr, P->d_S.get(), K, w, s);
+        std::vector<int32_t> fo(nr);
+        for (int r = 0; r < nr; ++r) fo[r] = r / nvec;
+        DBuf<int32_t> dfo = to_device(P, fo.data(), fo.size(), DOT_HOST);
+        DBuf<double2> XP(P->arena, std::max<size_t>((size_t)nr * nP, 1));
+        solve_rhs(P, -1, nullptr, 1, nr, R.get(), dfo.get(), XP.get(), nullptr);
+        const int n_side = side == 0 ? P->n_src : P->n_det;
+        launch_gather_cols(nf, nvec, n_side, XP.get(), (size_t)nvec * nP, nP,
+                           side == 0 ? P->d_src_slot.get() : P->d_det_slot.get(), out, (size_t)nvec * n_side, n_side, s);
+        P->stats.kernel_launches += 2;
+        if (side == 0) {     // b_s^T x = theta_s / (hx hy hz) x[src_s]  (reading R6)
+            std::vector<double2> h((size_t)nr * n_side);
+            DOT_CUDA_TRY(cudaMemcpyAsync(h.data(), out, h.size() * sizeof(double2), cudaMemcpyDeviceToHost, s));
+            sync(P);
+            for (int r = 0; r < nr; ++r)
+                for (int a = 0; a < n_side; ++a) {
+                    double2& v = h[(size_t)r * n_side + a];
+                    v.x *= P->src_scale[a];
+                    v.y *= P->src_scale[a];
+                }
+            DOT_CUDA_TRY(cudaMemcpyAsync(out, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+        }
+        sync(P);
+    };
+    OptContext oc{P->arena, P->stream, P->n_freq, P->n_src, P->n_det, P->n_p, P->K, P->nP,
+                  nullptr, nullptr, P->d_S_slot.get(), P->d_G.get(), &P->stats.kernel_launches};
+    double obj = optimize_two_phase_subspace(oc, ops, k, iters, block, hW, ls, hV, ld, hXs, hXd);
     if (objective_out) *objective_out = obj;
     if (where == DOT_HOST) {
         std::memcpy(W_out, hW.data(), hW.size() * sizeof(double));

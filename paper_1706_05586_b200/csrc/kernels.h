@@ -122,7 +122,13 @@ void launch_gather_cols(int nb, int rows, int ncols, const double2* X, size_t xb
 void launch_csub_inplace(double2* a, const double2* b, size_t n, cudaStream_t s);
 // *out = sum |a[i]|^2 (deterministic, single launch)
 void launch_sumsq(const double2* a, size_t n, double* out, cudaStream_t s);
-// x[i] *= 1 (real diagonal weights): y[b][i] = x[b][i] * w[i]
+// Dt[f][s][d] = D[f][d][s]
 void launch_transpose_data(const double2* D, int nf, int nd, int ns, double2* Dt, cudaStream_t s);
+
+// R[r][S[x]] = w[r][x], r < nr (dense right-hand sides supported on S)
+void launch_scatter_support(double2* R, size_t N, int nr, const int32_t* S, int K, const double2* w, cudaStream_t s);
+// w[f][q][x] = sum_i Z[f][i][x] sum_k C[f][q][i][k] G[x][k]   (C [nf][nq][ncol][n_p], Z [nf][ncol][K])
+void launch_form_support_rhs(int nf, int nq, int K, int ncol, int n_p, const double2* C, const double2* Z,
+                             const double* G, double2* w, cudaStream_t s);
 
 }  // namespace dot

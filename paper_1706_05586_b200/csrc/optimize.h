@@ -1,5 +1,6 @@
 // Simultaneous optimized sources and detectors (Sec. 3.2, Sec. 3.3.2).
 #pragma once
+#include <functional>
 #include <vector>
 
 #include "arena.h"
@@ -21,6 +22,27 @@ struct OptContext {
 // Two-phase alternating replacement of k directions; W (ns x ls) and V (nd x ld)
 // row-major host matrices, updated in place.  Returns ||(W^T (x) V^T) J||_F^2.
 double optimize_two_phase(OptContext& c, int k, std::vector<double>& W, int ls, std::vector<double>& V, int ld);
+
+// Solver callbacks of the matrix-free (subspace-iteration) variant, provided by the
+// C-ABI layer (they run the batched COCG kernels):
+struct SubspaceOps {
+    // fields of point combinations on the support S: side 0 = B coeff (sources), 1 = C coeff
+    // (detectors); coeff host [n_side][ncols] row-major; out device [nf][ncols][K]
+    std::function<void(int side, const std::vector<double>& coeff, int ncols, double2* out)> fields;
+    // solve A_f x = w_f for nvec right-hand sides supported on S (w device [nf][nvec][K]) and
+    // return b_s^T x (side 0, sources; b_s = theta e_s / cell volume) or c_d^T x (side 1):
+    // out device [nf][nvec][n_side]
+    std::function<void(const double2* w, int nvec, int side, double2* out)> solve_support;
+};
+
+// Two-phase replacement where the add steps (Theorems 3.7, 3.6) use `iters` steps of
+// subspace iteration with a `blk`-vector block (reading R16) applied
+// matrix-free (2 n_freq solves per block vector per step); the remove steps use the
+// sketched Jacobian of the current W, V.  X0s [ns][k*blk], X0d [nd][k*blk]: add step t
+// starts from columns t*blk .. (t+1)*blk - 1.
+double optimize_two_phase_subspace(OptContext& c, SubspaceOps& ops, int k, int iters, int blk,
+                                   std::vector<double>& W, int ls, std::vector<double>& V, int ld,
+                                   const std::vector<double>& X0s, const std::vector<double>& X0d);
 
 // Host symmetric eigen-decomposition (Householder tridiagonalisation + implicit
 // QL); eigenvalues descending in w, eigenvectors as columns of Z (row-major n x n).

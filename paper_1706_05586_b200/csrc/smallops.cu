@@ -68,6 +68,34 @@ __global__ void transpose_data_kernel(const double2* D, int nf, int nd, int ns, 
     }
 }
 
+// R[r][S[x]] = w[r][x]  (dense right-hand sides supported on S)
+__global__ void scatter_support_kernel(double2* R, size_t N, int K, const int32_t* S, const double2* w) {
+    const int r = blockIdx.y;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < K; x += gridDim.x * blockDim.x)
+        R[(size_t)r * N + S[x]] = w[(size_t)r * K + x];
+}
+
+// w[f][q][x] = sum_i Z[f][i][x] sum_k C[f][q][i][k] G[x][k]
+__global__ void form_support_rhs_kernel(int K, int ncol, int n_p, int nq, const double2* __restrict__ C,
+                                        const double2* __restrict__ Z, const double* __restrict__ G, double2* w) {
+    const int q = blockIdx.y, f = blockIdx.z;
+    const double2* Cf = C + ((size_t)f * nq + q) * ncol * n_p;
+    const double2* Zf = Z + (size_t)f * ncol * K;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < K; x += gridDim.x * blockDim.x) {
+        const double* g = G + (size_t)x * n_p;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int i = 0; i < ncol; ++i) {
+            double2 c = make_double2(0.0, 0.0);
+            for (int k = 0; k < n_p; ++k) {
+                c.x = fma(Cf[(size_t)i * n_p + k].x, g[k], c.x);
+                c.y = fma(Cf[(size_t)i * n_p + k].y, g[k], c.y);
+            }
+            acc = cfma(c, Zf[(size_t)i * K + x], acc);
+        }
+        w[((size_t)f * nq + q) * K + x] = acc;
+    }
+}
+
 inline unsigned blocks_for(size_t n) {
     size_t g = (n + 255) / 256;
     return (unsigned)std::max<size_t>(1, std::min<size_t>(g, 8192));
@@ -105,6 +133,21 @@ void launch_sumsq(const double2* a, size_t n, double* out, cudaStream_t s) {
 
 void launch_transpose_data(const double2* D, int nf, int nd, int ns, double2* Dt, cudaStream_t s) {
     transpose_data_kernel<<<blocks_for((size_t)nf * nd * ns), 256, 0, s>>>(D, nf, nd, ns, Dt);
+    DOT_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_scatter_support(double2* R, size_t N, int nr, const int32_t* S, int K, const double2* w, cudaStream_t s) {
+    if (nr <= 0 || K <= 0) return;
+    dim3 grid((unsigned)std::min((K + 255) / 256, 1024), nr);
+    scatter_support_kernel<<<grid, 256, 0, s>>>(R, N, K, S, w);
+    DOT_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_form_support_rhs(int nf, int nq, int K, int ncol, int n_p, const double2* C, const double2* Z,
+                             const double* G, double2* w, cudaStream_t s) {
+    if (nf <= 0 || nq <= 0 || K <= 0) return;
+    dim3 grid((unsigned)std::min((K + 127) / 128, 1024), nq, nf);
+    form_support_rhs_kernel<<<grid, 128, 0, s>>>(K, ncol, n_p, nq, C, Z, G, w);
     DOT_CUDA_TRY(cudaGetLastError());
 }
 

@@ -237,6 +237,52 @@ def test_optimize_directions_parity(dot):
         assert np.allclose(np.linalg.norm(Wg[:, -1]), 3.0)
 
 
+@pytest.mark.parametrize("iters,block", [(1, 2), (5, 2), (3, 1)])
+def test_optimize_directions_subspace_parity(dot, iters, block):
+    """Matrix-free subspace-iteration replacement (reading R16) against the oracle's
+    explicit subspace iteration: same W, V, starting blocks and iteration count."""
+    from oracle import frob_objective, optimize_directions_subspace
+    cfg = small_config(n=(12, 12, 8), L=(4.0, 4.0, 3.0), src=(4, 3), det=(3, 3), eps=0.5)
+    prob, wl = small_problem(cfg, with_data=False)
+    g = gpu_problem(dot, cfg, prob, wl)
+    rng = np.random.default_rng(21)
+    ns, nd = 12, 9
+    W = np.sign(rng.standard_normal((ns, 4)))
+    V = np.sign(rng.standard_normal((nd, 3)))
+    X0s_all, X0d_all = rng.standard_normal((ns, 2 * block)), rng.standard_normal((nd, 2 * block))
+    for k in (1, 2):
+        X0s, X0d = X0s_all[:, :k * block], X0d_all[:, :k * block]
+        g.reset_stats()
+        Wg, Vg, obj = g.optimize_directions_subspace(k, W, V, X0s, X0d, iters=iters)
+        st = g.stats()
+        Wr, Vr = optimize_directions_subspace(prob, wl.p, W, V, k, iters, X0s, X0d)
+        objr = frob_objective(jacobian(prob, wl.p, Wr, Vr))
+        assert abs(obj - objr) <= 1e-7 * objr
+        # removed-and-kept columns span the same space; added columns match exactly (sign rule)
+        for A, B in ((Wg, Wr), (Vg, Vr)):
+            Qa, _ = np.linalg.qr(A[:, :-k])
+            Qb, _ = np.linalg.qr(B[:, :-k])
+            assert np.abs(Qa @ Qa.T - Qb @ Qb.T).max() < 1e-7
+            assert np.abs(A[:, -k:] - B[:, -k:]).max() <= 1e-6 * np.abs(B[:, -k:]).max()
+        # solve accounting: W and V fields once, then 2 solves per block vector per step per frequency
+        nf = len(cfg.freqs_hz)
+        assert st["rhs_solved"] == nf * (4 + 3) + 2 * k * iters * 2 * block * nf
+
+
+def test_optimize_directions_subspace_converges_to_exact(dot):
+    cfg = small_config(n=(12, 12, 8), L=(4.0, 4.0, 3.0), src=(4, 3), det=(3, 3), eps=0.5)
+    prob, wl = small_problem(cfg, with_data=False)
+    g = gpu_problem(dot, cfg, prob, wl)
+    rng = np.random.default_rng(5)
+    W = np.sign(rng.standard_normal((12, 4)))
+    V = np.sign(rng.standard_normal((9, 3)))
+    We, Ve, oe = g.optimize_directions(1, W, V)
+    Ws, Vs, os_ = g.optimize_directions_subspace(1, W, V, rng.standard_normal((12, 2)), rng.standard_normal((9, 2)),
+                                                 iters=60)
+    assert abs(os_ - oe) <= 1e-8 * oe
+    assert abs(float(Ws[:, -1] @ We[:, -1])) / 12 > 1 - 1e-8
+
+
 RING = dict(DOT_COCG_KERNEL="ring")
 KNOBS = [dict(RING, DOT_COCG_THREADS="256"), dict(RING, DOT_COCG_THREADS="128"),
          dict(RING, DOT_COCG_SMEM_KB="64"), dict(RING, DOT_COCG_PREFETCH="2"),

@@ -205,7 +205,7 @@ def test_optimize_directions_subspace_matches_exact_when_converged():
     prob, wl = small_problem(cfg, with_data=False)
     rng = np.random.default_rng(3)
     W, V = np.sign(rng.standard_normal((6, 3))), np.sign(rng.standard_normal((6, 3)))
-    X0s, X0d = rng.standard_normal((6, 2)), rng.standard_normal((6, 2))
+    X0s, X0d = rng.standard_normal((6, 2)), rng.standard_normal((6, 2))   # s = 1: one block of 2
     We, Ve = optimize_directions(prob, wl.p, W, V, 1)
     Ws, Vs = optimize_directions_subspace(prob, wl.p, W, V, 1, 300, X0s, X0d)
     # kept columns identical (same remove steps); new columns equal up to sign
