@@ -62,6 +62,7 @@ struct dot_problem {
     bool timing = false;
     std::vector<cudaEvent_t> events;
     int* h_count = nullptr;
+    int num_sms = 148;
 
     ~dot_problem() {
         for (auto e : events) cudaEventDestroy(e);
@@ -128,7 +129,8 @@ std::vector<double> host_copy(dot_problem* P, const double* src, size_t count, i
 
 size_t per_rhs_bytes(const dot_problem* P) {
     const size_t vec = P->N * sizeof(double2);
-    return 4 * vec + 2 * P->tl.ntiles * kNumPartials * sizeof(double) + 2 * sizeof(RhsState) +
+    const size_t zmax = (size_t)std::max(1, P->nz / 4);
+    return 4 * vec + 2 * P->tl.ntiles * zmax * kNumPartials * sizeof(double) + 2 * sizeof(RhsState) +
            sizeof(double) + 4 * Arena::kAlign;
 }
 
@@ -144,18 +146,36 @@ std::vector<int32_t> solve_rhs(dot_problem* P, int side, const double* d_coeff, 
     std::vector<int32_t> iters(n_rhs, 0);
     if (n_rhs == 0) return iters;
     const size_t N = P->N;
-    const size_t prb = per_rhs_bytes(P) + (Xfull ? 0 : 0);
+    const size_t prb = per_rhs_bytes(P);
     size_t fit = P->arena.largest_free() / prb;
     // multiple allocations fragment the arena: keep a safety margin
     fit = fit > 2 ? fit - 1 : fit;
     if (fit < 1) throw Error(DOT_ERR_WORKSPACE, "workspace too small for one right-hand side");
     const int chunk = (int)std::min<size_t>(fit, (size_t)n_rhs);
     const int CHK = 8;
+    // z chunks (z pass): enough CTAs to fill the GPU when few RHS iterate together
+    // (DESIGN.md "z chunks"); at least 8 planes per chunk.  DOT_COCG_ZCHUNKS overrides.
+    auto zchunks = [&](int nb) {
+        if (P->tl.kind != 1) return 1;
+        int n = 1;
+        const char* e = std::getenv("DOT_COCG_ZCHUNKS");
+        if (e) {
+            n = std::min(std::max(1, std::atoi(e)), std::max(1, P->nz / 4));
+        } else {
+            const long long target = 4LL * P->num_sms;
+            const long long have = (long long)P->tl.ntiles * nb;
+            if (have < target) n = (int)((target + have - 1) / have);
+            n = std::min(n, std::max(1, P->nz / 8));
+        }
+        const int zlen = (P->nz + n - 1) / n;
+        return (P->nz + zlen - 1) / zlen;
+    };
 
     for (int r0 = 0; r0 < n_rhs; r0 += chunk) {
         const int nb = std::min(chunk, n_rhs - r0);
         DBuf<double2> R0(P->arena, nb * N), R1(P->arena, nb * N), P0(P->arena, nb * N), P1(P->arena, nb * N);
-        DBuf<double> part(P->arena, 2 * (size_t)nb * P->tl.ntiles * kNumPartials);
+        const int nzch = zchunks(nb);
+        DBuf<double> part(P->arena, 2 * (size_t)nb * P->tl.ntiles * nzch * kNumPartials);
         DBuf<RhsState> st(P->arena, 2 * (size_t)nb);
         DBuf<double> shift(P->arena, nb);
 
@@ -203,7 +223,9 @@ std::vector<int32_t> solve_rhs(dot_problem* P, int side, const double* d_coeff, 
         a.Pv[0] = P0.get();
         a.Pv[1] = P1.get();
         a.part[0] = part.get();
-        a.part[1] = part.get() + (size_t)nb * P->tl.ntiles * kNumPartials;
+        a.part[1] = part.get() + (size_t)nb * P->tl.ntiles * nzch * kNumPartials;
+        a.nzch = nzch;
+        a.zlen = (P->nz + nzch - 1) / nzch;
         a.st[0] = st.get();
         a.st[1] = st.get() + nb;
         a.samp_nodes = P->d_P.get();
@@ -441,6 +463,11 @@ int dot_create(const dot_config* cfg, dot_problem** out) {
         P->pc = PalsConst{P->nx, P->ny, P->nz, P->n_rbf, P->hx, P->hy, P->hz, P->gamma, P->eps, P->cutoff,
                           P->mua_in, P->mua_out};
         DOT_CUDA_TRY(cudaMallocHost(&P->h_count, sizeof(int)));
+        {
+            int dev = 0;
+            DOT_CUDA_TRY(cudaGetDevice(&dev));
+            DOT_CUDA_TRY(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, dev));
+        }
         *out = p.release();
         return DOT_OK;
     } catch (const Error& e) {

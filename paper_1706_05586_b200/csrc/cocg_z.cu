@@ -47,7 +47,7 @@ struct ZScalars {
 // tiles, fixed-order butterfly reduction: identical in every CTA of the RHS).
 __device__ void zpass_scalars(const PassArgs& a, int rhs, int tile, ZScalars* out) {
     const int lane = threadIdx.x & 31;
-    const int ntiles = a.tl.ntiles;
+    const int ntiles = a.tl.ntiles * a.nzch;          // partial slots per RHS (tiles x z chunks)
     const double* pp = a.part[a.k & 1] + (size_t)rhs * ntiles * kNumPartials;
     double s[kNumPartials];
 #pragma unroll
@@ -147,15 +147,22 @@ __device__ __forceinline__ double2 stencil_int(const OpConst& op, double shift, 
 // (mu rides along in the same bulk-copy group when MUT; else it is loaded per thread).
 // RPT: slot rows per thread (a thread owns rows RPT*m .. RPT*m + RPT - 1 of one column; the
 // y-neighbours inside its strip come from registers).
-template <bool FULLX, int MAXT, int MINB, int NS, bool MUT, int RPT>
+template <bool FULLX, int MAXT, int MINB, int NS, bool MUT, int RPT, bool ZC>
 __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int LPD = 4;                              // L2 prefetch distance (planes)
     constexpr int PD = NS - 2;                          // TMA planes in flight
-    const int tile = blockIdx.x, rhs = blockIdx.y;
+    const int ntiles = a.tl.ntiles;
+    const int tile = blockIdx.x % ntiles, zc = blockIdx.x / ntiles, rhs = blockIdx.y;
     const int nx = a.op.nx, ny = a.op.ny, nz = a.op.nz;
     const int TY = a.tl.TY;
-    const int ntiles = a.tl.ntiles;
+    // z chunk [z0, z1) of this CTA; phase 1 runs on [a1, b1), phase 2 on [a2, b2)
+    // (two / one halo planes recomputed on each side)
+    // (ZC = false: one chunk, the whole z range -- the bounds fold to constants)
+    const int z0 = ZC ? zc * a.zlen : 0, z1 = ZC ? min(nz, z0 + a.zlen) : nz;
+    const int a1 = ZC ? max(z0 - 2, 0) : 0, b1 = ZC ? min(z1 + 2, nz) : nz;
+    const int a2 = ZC ? max(z0 - 1, 0) : 0, b2 = ZC ? min(z1 + 1, nz) : nz;
+    const int fend = ZC ? min(b1, z1) + 2 : nz + 2;
     const int rowsP = TY + 4, rowsR = TY + 2;
     const int PS = nx * ny;
     const size_t N = (size_t)PS * nz;
@@ -171,7 +178,7 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
     int2* s_samp = reinterpret_cast<int2*>(scratch + 32 * kNumPartials);   // [nz] sample ranges
     __shared__ ZScalars sh_sc;
 
-    if (threadIdx.x < 32) zpass_scalars(a, rhs, tile, &sh_sc);
+    if (threadIdx.x < 32) zpass_scalars(a, rhs, blockIdx.x, &sh_sc);
     {   // zero the slot ring and Rbuf: rows outside the domain stay zero (Dirichlet y faces)
         const int tot = NS * slotW + 3 * rbE;
         for (int i = threadIdx.x; i < tot; i += blockDim.x) slots[i] = cmk(0, 0);
@@ -234,9 +241,9 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Pin + g), "r"(tile_bytes) : "memory");
     };
     if (threadIdx.x == 0)
-        for (int z = 0; z < PD && z < nz; ++z) issue(z, z);
+        for (int z = a1; z < a1 + PD && z < b1; ++z) issue(z, z - a1);
     if (threadIdx.x == 32)
-        for (int z = PD; z < PD + LPD && z < nz; ++z) prefetch_l2(z);
+        for (int z = a1 + PD; z < a1 + PD + LPD && z < b1; ++z) prefetch_l2(z);
 
     // ---- per-thread geometry: rows r0 .. r0 + RPT - 1 of column x
     const int t = threadIdx.x;
@@ -259,9 +266,9 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
     const int go = (j0 - 2 + r0) * nx + x;             // plane offset of row 0 (may be outside; unused then)
     const bool hasW = x > 0, hasE = x < nx - 1;
     // running per-thread global pointers (advance one plane per step)
-    double2* pP = a.Pv[kout] + (size_t)rhs * N + go;                       // p_k at plane f
-    double2* pR = a.R[kout] + (size_t)rhs * N + go - 2 * (ptrdiff_t)PS;    // r_{k+1} at plane f - 2
-    double2* pX = FULLX ? a.X + (size_t)rhs * N + go : nullptr;
+    double2* pP = a.Pv[kout] + (size_t)rhs * N + go + (ptrdiff_t)a1 * PS;        // p_k at plane f
+    double2* pR = a.R[kout] + (size_t)rhs * N + go + (ptrdiff_t)(a1 - 2) * PS;   // r_{k+1} at plane f - 2
+    double2* pX = FULLX ? a.X + (size_t)rhs * N + go + (ptrdiff_t)a1 * PS : nullptr;
     const double* pMu = a.mu + go;                     // used when !MUT
 
     double acc[kNumPartials];
@@ -290,9 +297,10 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
         constexpr int i0 = decltype(IDX)::v;           // f % 3
         constexpr int i1 = (i0 + 2) % 3;               // (f - 1) % 3
         constexpr int i2 = (i0 + 1) % 3;               // (f - 2) % 3
-        if (threadIdx.x == 0 && f + PD < nz) issue(f + PD, sl_iss);
-        if (threadIdx.x == 32 && f + PD + LPD < nz) prefetch_l2(f + PD + LPD);
-        if (!MUT && f < nz)
+        if (threadIdx.x == 0 && f + PD < b1) issue(f + PD, sl_iss);
+        if (threadIdx.x == 32 && f + PD + LPD < b1) prefetch_l2(f + PD + LPD);
+        const bool ownf = !ZC || (f >= z0 && f < z1);
+        if (!MUT && f < b1)
 #pragma unroll
             for (int j = 0; j < RPT; ++j)
                 if (ph2[j]) MU[j][i0] = pMu[(size_t)f * PS + j * nx];
@@ -300,7 +308,7 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
         double2 pf[RPT];
 #pragma unroll
         for (int j = 0; j < RPT; ++j) pf[j] = z2;
-        if (f < nz) {
+        if (f < b1) {
             asm volatile(
                 "{\n\t.reg .pred p;\n\t"
                 "WAITZ_%=:\n\t"
@@ -317,7 +325,7 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
                     const double2 rf = sr[j * nx];
                     pf[j] = first ? rf : cfma(beta, sr[slotE + j * nx], rf);
                     sr[slotE + j * nx] = pf[j];
-                    if (own[j]) {
+                    if (own[j] && ownf) {
                         pP[j * nx] = pf[j];
                         if (FULLX) pX[j * nx] = cfma(sh_sc.alpha, pf[j], pX[j * nx]);
                     }
@@ -333,7 +341,8 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
             mug[j] = 0.0;
         }
         const int g = f - 1;
-        if (g >= 0 && g < nz) {
+        if (g >= a2 && g < b2) {
+            const bool owng = !ZC || (g >= z0 && g < z1);
             const double2* sr = slots + sl_prev * slotW;
             const double2* sp = sr + slotE;
             if (any2) {
@@ -357,7 +366,7 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
                         qv = stencil(ce, mug[j], pc, cadd(xw, xe), cadd(ys, yn), Pq[j][i2], pf[j]);
                     rng[j] = csub(sr[oj], cmul(alpha, qv));
                     rbuf[i1 * rbE + o3 + j * nx] = rng[j];
-                    if (own[j]) {
+                    if (own[j] && owng) {
                         acc[4] = fma(rng[j].x, qv.x, fma(-rng[j].y, qv.y, acc[4]));
                         acc[5] = fma(rng[j].x, qv.y, fma(rng[j].y, qv.x, acc[5]));
                         acc[6] = fma(pc.x, qv.x, fma(-pc.y, qv.y, acc[6]));
@@ -365,7 +374,7 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
                     }
                 }
             }
-            if (!FULLX && a.nP > 0) {
+            if (!FULLX && a.nP > 0 && owng) {
                 const int2 sr2 = s_samp[g];
                 if (sr2.x < sr2.y) {
                     double2* XP = a.XP + (size_t)rhs * a.nP;
@@ -380,7 +389,7 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
         for (int j = 0; j < RPT; ++j) Pq[j][i0] = pf[j];
         // ---- phase 3: plane tt = f - 2
         const int tt = f - 2;
-        if (any_own && tt >= 0) {
+        if (any_own && tt >= z0 && tt < z1) {
             const double2* rc = rbuf + i2 * rbE + o3;
             const bool interior = tt > 0 && tt < nz - 1;
             const PlaneCoef ce = interior ? PlaneCoef{} : plane_coef(a.op, tt, shift);
@@ -425,10 +434,10 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
     };
     // RN[.][i0] read in phase 3 is r_{k+1}(f-3), written three steps earlier.
 #pragma unroll 1
-    for (int f = 0; f < nz + 2; f += 3) {
+    for (int f = a1; f < fend; f += 3) {
         step(f, IC<0>());
-        if (f + 1 < nz + 2) step(f + 1, IC<1>());
-        if (f + 2 < nz + 2) step(f + 2, IC<2>());
+        if (f + 1 < fend) step(f + 1, IC<1>());
+        if (f + 2 < fend) step(f + 2, IC<2>());
     }
     // ---- deterministic block reduction of the partials
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
@@ -441,7 +450,7 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
     if (threadIdx.x < kNumPartials) {
         double sum = 0;
         for (int w = 0; w < nw; ++w) sum += scratch[w * kNumPartials + threadIdx.x];
-        a.part[kout][((size_t)rhs * ntiles + tile) * kNumPartials + threadIdx.x] = sum;
+        a.part[kout][((size_t)rhs * ntiles * a.nzch + blockIdx.x) * kNumPartials + threadIdx.x] = sum;
     }
 }
 
@@ -449,14 +458,19 @@ template <bool FX, int MAXT, int MINB, int NS, int RPT>
 void launch_z_ns(const PassArgs& a, int nb, cudaStream_t s) {
     // mu rides in the bulk-copy group when every copy is 16-byte sized and aligned
     const bool mut = (a.op.nx % 2 == 0);
-    auto k = mut ? cocg_zpass_kernel<FX, MAXT, MINB, NS, true, RPT> : cocg_zpass_kernel<FX, MAXT, MINB, NS, false, RPT>;
-    static size_t attr[2] = {0, 0};
-    if (attr[mut] < a.tl.smem) {
+    const bool zc = a.nzch > 1;
+    auto k = mut ? (zc ? cocg_zpass_kernel<FX, MAXT, MINB, NS, true, RPT, true>
+                       : cocg_zpass_kernel<FX, MAXT, MINB, NS, true, RPT, false>)
+                 : (zc ? cocg_zpass_kernel<FX, MAXT, MINB, NS, false, RPT, true>
+                       : cocg_zpass_kernel<FX, MAXT, MINB, NS, false, RPT, false>);
+    static size_t attr[4] = {0, 0, 0, 0};
+    const int ai = (mut ? 1 : 0) + (zc ? 2 : 0);
+    if (attr[ai] < a.tl.smem) {
         DOT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.tl.smem));
-        attr[mut] = a.tl.smem;
+        attr[ai] = a.tl.smem;
     }
-    dim3 grid(a.tl.ntiles, nb);
-    launch_clustered(k, grid, a.tl.threads, a.tl.smem, s, a.tl.cluster, a);
+    dim3 grid(a.tl.ntiles * a.nzch, nb);
+    launch_clustered(k, grid, a.tl.threads, a.tl.smem, s, a.nzch == 1 ? a.tl.cluster : 1, a);
 }
 
 template <bool FX, int MAXT, int MINB, int RPT>

@@ -28,6 +28,8 @@ struct PassArgs {
     OpConst op;
     CocgTiling tl;
     int k = 0;                    // pass index
+    int nzch = 1;                 // z chunks per (tile, RHS) (z pass only; partial slots = ntiles * nzch)
+    int zlen = 0;                 // planes per z chunk
     int max_iter = 0;
     double tol2 = 0;              // tol^2
     const double* mu = nullptr;   // [N] absorption

@@ -283,6 +283,33 @@ def test_optimize_directions_subspace_converges_to_exact(dot):
     assert abs(float(Ws[:, -1] @ We[:, -1])) / 12 > 1 - 1e-8
 
 
+@pytest.mark.parametrize("knobs", [dict(DOT_COCG_ZCHUNKS="1"), dict(DOT_COCG_ZCHUNKS="2"),
+                                   dict(DOT_COCG_ZCHUNKS="3"), dict(DOT_COCG_ZCHUNKS="4"),
+                                   dict(DOT_COCG_ZCHUNKS="3", DOT_COCG_ZOPT="B"),
+                                   dict(DOT_COCG_ZCHUNKS="4", DOT_COCG_ZOPT="D", DOT_COCG_TY="5")])
+def test_z_chunks_keep_parity(dot, knobs, monkeypatch):
+    """z-chunked passes (each chunk recomputes 2 halo planes of p and 1 of r_{k+1},
+    DESIGN.md "z chunks") solve the same systems: nz = 19 splits into 10+9, 7+7+5, 5+5+5+4."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    cfg = small_config(n=(24, 20, 19), L=(4.0, 3.5, 3.0), src=(3, 2), det=(2, 3), eps=0.4)
+    prob, wl = small_problem(cfg, with_data=True)
+    g = gpu_problem(dot, cfg, prob, wl)
+    N = prob.grid.N
+    rng = np.random.default_rng(4)
+    b = rng.standard_normal((2, N)) + 1j * rng.standard_normal((2, N))
+    mu = absorption(wl.p, prob.grid, cfg)
+    x, _ = g.solve(b, 1)
+    ref = spla.splu(prob.operator(mu, 1).tocsc()).solve(b.T).T
+    assert rel(x, ref) < 1e-11
+    X = g.solve_sampled(0)
+    samp = g.samples()
+    M = np.transpose(X[:, :, np.searchsorted(samp, wl.det_nodes)], (0, 2, 1))
+    assert rel(M, measurements(prob, wl.p)) < 1e-8
+    J = g.jacobian(None, None)
+    assert rel(J, jacobian(prob, wl.p, np.eye(cfg.n_s), np.eye(cfg.n_d))) < 1e-7
+
+
 RING = dict(DOT_COCG_KERNEL="ring")
 KNOBS = [dict(RING, DOT_COCG_THREADS="256"), dict(RING, DOT_COCG_THREADS="128"),
          dict(RING, DOT_COCG_SMEM_KB="64"), dict(RING, DOT_COCG_PREFETCH="2"),
@@ -291,7 +318,8 @@ KNOBS = [dict(RING, DOT_COCG_THREADS="256"), dict(RING, DOT_COCG_THREADS="128"),
          dict(DOT_COCG_ZOPT="A"), dict(DOT_COCG_ZOPT="B"), dict(DOT_COCG_ZOPT="C"),
          dict(DOT_COCG_PREFETCH="1"), dict(DOT_COCG_PREFETCH="3"), dict(DOT_COCG_TY="3"), dict(DOT_COCG_TY="5"),
          dict(DOT_COCG_TY="4", DOT_COCG_CLUSTER="2"), dict(DOT_COCG_ZOPT="D"),
-         dict(DOT_COCG_ZOPT="D", DOT_COCG_TY="5"), dict(DOT_COCG_ZOPT="D", DOT_COCG_TY="3", DOT_COCG_PREFETCH="1")]
+         dict(DOT_COCG_ZOPT="D", DOT_COCG_TY="5"), dict(DOT_COCG_ZOPT="D", DOT_COCG_TY="3", DOT_COCG_PREFETCH="1"),
+]
 
 
 @pytest.mark.parametrize("knobs", KNOBS)
