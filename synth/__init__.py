@@ -13,6 +13,7 @@ from .generate import (  # noqa: F401
     draw_params,
     rademacher,
     noise_draws,
+    subspace_start,
     Workload,
     make_workload,
 )

@@ -53,6 +53,12 @@ def rademacher(n: int, l: int, seed: int, stream: int = 0) -> np.ndarray:
     return (2.0 * rng.integers(0, 2, size=(n, l)) - 1.0).astype(np.float64)
 
 
+def subspace_start(n: int, cols: int, seed: int, stream: int) -> np.ndarray:
+    """Standard-normal starting blocks of the subspace iteration (reading R16)."""
+    rng = np.random.Generator(np.random.PCG64([seed, 100 + stream]))
+    return rng.standard_normal((n, cols))
+
+
 def noise_draws(seed: int, shape) -> np.ndarray:
     """Complex standard normal draws (xi + i eta)/sqrt(2) for the data noise."""
     rng = np.random.Generator(np.random.PCG64([seed, 7]))
@@ -71,6 +77,8 @@ class Workload:
     W: Optional[np.ndarray]      # (n_s, ls) Rademacher or None (identity)
     V: Optional[np.ndarray]      # (n_d, ld) Rademacher or None (identity)
     xi: np.ndarray               # (n_freq, n_d, n_s) complex noise draws
+    X0_src: Optional[np.ndarray] = None   # (n_s, n_opt * block) subspace-iteration starts
+    X0_det: Optional[np.ndarray] = None   # (n_d, n_opt * block)
 
     @property
     def p_true_padded(self):
@@ -101,4 +109,8 @@ def make_workload(cfg: DOTConfig) -> Workload:
     W = rademacher(cfg.n_s, cfg.ls, cfg.sketch_seed, 0) if cfg.ls else None
     V = rademacher(cfg.n_d, cfg.ld, cfg.sketch_seed, 1) if cfg.ld else None
     xi = noise_draws(cfg.seed, (cfg.n_freq, cfg.n_d, cfg.n_s))
-    return Workload(cfg, src, det, p, p_true, W, V, xi)
+    X0s = X0d = None
+    if cfg.n_opt:
+        X0s = subspace_start(cfg.n_s, 2 * cfg.n_opt, cfg.sketch_seed, 0)    # block size 2
+        X0d = subspace_start(cfg.n_d, 2 * cfg.n_opt, cfg.sketch_seed, 1)
+    return Workload(cfg, src, det, p, p_true, W, V, xi, X0s, X0d)
