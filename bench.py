@@ -246,7 +246,7 @@ def main():
         X0d = torch.as_tensor(wl.X0_det, device=dev) if wl.X0_det is not None else None
 
         def run_step(p, W, V, data=None):
-            """configs[1] (sketch32): set_params, misfit(W,V), jacobian(W,V).
+            """configs[1] (sketch32): set_params, jacobian(W,V), misfit(W,V).
             configs[3] (opt96): the same, then replace n_opt random directions by optimized
             ones (5 subspace iterations, block 2; reading R16) and evaluate the reduced
             problem (misfit, jacobian) with the new W, V."""
@@ -254,16 +254,16 @@ def main():
             if data is not None:
                 gp.set_data(data)
             gp.set_params(p)
-            m = gp.misfit(W, V)
-            J = gp.jacobian(W, V, where=0 if host else 1)
+            J = gp.jacobian(W, V, where=0 if host else 1)     # forward W + adjoint V solves in one batch
+            m = gp.misfit(W, V)                                 # cached forward fields
             d2h = J.nbytes + 8 if host else 0
             if cfg.n_opt:
                 xs = wl.X0_src if host else X0s
                 xd = wl.X0_det if host else X0d
                 W2, V2, obj = gp.optimize_directions_subspace(cfg.n_opt, W, V, xs, xd,
                                                               iters=cfg.n_subspace_iters)
-                m = gp.misfit(W2, V2)
                 J = gp.jacobian(W2, V2, where=0 if host else 1)
+                m = gp.misfit(W2, V2)
                 d2h += J.nbytes + 8 + 8 + W2.nbytes + V2.nbytes if host else 0
             return {"misfit": m, "J_sketch": J, "d2h_bytes": d2h}
 

@@ -140,9 +140,30 @@ size_t per_rhs_bytes(const dot_problem* P) {
 // or, if dense != null, the dense vector dense[r].  Outputs: XP [n_rhs][nP]
 // (sampled) or, if Xfull != null, Xfull [n_rhs][N].  freq_of: optional per-RHS
 // frequency (dense mode).  Returns per-RHS iterations.
+// One segment of point-combination right-hand sides: RHS (f, c) = side's point
+// combination with coefficient column c at frequency f, f-major (nf * ncols RHS).
+struct Seg {
+    int side;
+    const double* d_coeff;   // device [n_side][ncols] or null (identity)
+    int ncols;
+};
+
+std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, int n_rhs, const double2* dense,
+                                 const int32_t* d_freq_of, double2* XP, double2* Xfull);
+
 std::vector<int32_t> solve_rhs(dot_problem* P, int side, const double* d_coeff, int ncols, int n_rhs,
                                const double2* dense, const int32_t* d_freq_of, double2* XP,
                                double2* Xfull) {
+    std::vector<Seg> segs;
+    if (!dense) segs.push_back(Seg{side, d_coeff, ncols});
+    return solve_batch(P, segs, n_rhs, dense, d_freq_of, XP, Xfull);
+}
+
+// Batched solve of the concatenated RHS lists of `segs` (point mode) or of the dense
+// vectors `dense` (with per-RHS frequency d_freq_of).  All RHS iterate together in
+// chunks of what fits the workspace.
+std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, int n_rhs, const double2* dense,
+                                 const int32_t* d_freq_of, double2* XP, double2* Xfull) {
     std::vector<int32_t> iters(n_rhs, 0);
     if (n_rhs == 0) return iters;
     const size_t N = P->N;
@@ -185,10 +206,21 @@ std::vector<int32_t> solve_rhs(dot_problem* P, int side, const double* d_coeff, 
                                          cudaMemcpyDeviceToDevice, P->stream));
         } else {
             DOT_CUDA_TRY(cudaMemsetAsync(R0.get(), 0, (size_t)nb * N * sizeof(double2), P->stream));
-            const int nn = side == 0 ? P->n_src : P->n_det;
-            launch_scatter_rhs(R0.get(), N, nb, r0, ncols, side == 0 ? P->d_src.get() : P->d_det.get(), nn,
-                               d_coeff, side == 0 ? P->d_src_scale.get() : P->d_det_scale.get(), P->stream);
-            P->stats.kernel_launches++;
+            long long gs = 0;
+            for (const Seg& sg : segs) {                 // the part of each segment inside [r0, r0 + nb)
+                const long long ge = gs + (long long)P->n_freq * sg.ncols;
+                const long long rs = std::max<long long>(r0, gs), re = std::min<long long>(r0 + nb, ge);
+                if (rs < re) {
+                    const int nn = sg.side == 0 ? P->n_src : P->n_det;
+                    launch_scatter_rhs(R0.get() + (size_t)(rs - r0) * N, N, (int)(re - rs), rs - gs, sg.ncols,
+                                       sg.side == 0 ? P->d_src.get() : P->d_det.get(), nn, sg.d_coeff,
+                                       sg.side == 0 ? P->d_src_scale.get() : P->d_det_scale.get(), P->stream);
+                    launch_fill_shift(shift.get() + (rs - r0), (int)(re - rs), rs - gs, sg.ncols,
+                                      P->d_omega_nu.get(), P->stream);
+                    P->stats.kernel_launches += 2;
+                }
+                gs = ge;
+            }
         }
         if (d_freq_of) {
             // shift[r] = omega_nu[freq_of[r0 + r]] : reuse fill_shift with ncols = 1 on a gathered table
@@ -204,9 +236,6 @@ std::vector<int32_t> solve_rhs(dot_problem* P, int side, const double* d_coeff, 
             DOT_CUDA_TRY(cudaMemcpyAsync(shift.get(), sh.data(), nb * sizeof(double), cudaMemcpyHostToDevice,
                                          P->stream));
             sync(P);
-        } else {
-            launch_fill_shift(shift.get(), nb, r0, ncols, P->d_omega_nu.get(), P->stream);
-            P->stats.kernel_launches++;
         }
         if (XP) DOT_CUDA_TRY(cudaMemsetAsync(XP + (size_t)r0 * P->nP, 0, (size_t)nb * P->nP * sizeof(double2), P->stream));
         if (Xfull) DOT_CUDA_TRY(cudaMemsetAsync(Xfull + (size_t)r0 * N, 0, (size_t)nb * N * sizeof(double2), P->stream));
@@ -287,71 +316,118 @@ std::vector<int32_t> solve_rhs(dot_problem* P, int side, const double* d_coeff, 
     return iters;
 }
 
+// ---------------------------------------------------------------- field caches
+// cache[side] holds sampled solutions [n_freq][ncols][nP] of one coefficient matrix
+// (identity, a selection, or a general combination).
+struct Req {
+    int side;
+    std::vector<double> hc;   // host [n_side][ncols]; empty for identity
+    bool identity;
+    int ncols;
+};
+
+// Can the fields of this request be served from the cache (directly or, for a
+// combination of cached point sources, by linear combination without solves)?
+bool cache_hit(dot_problem* P, const Req& q) {
+    const int n_side = q.side == 0 ? P->n_src : P->n_det;
+    const FieldCache& c = P->cache[q.side];
+    if (!c.valid) return false;
+    if (q.identity && c.identity) return true;
+    if (!q.identity && !c.identity && c.ncols == q.ncols && c.coeff == q.hc) return true;
+    if (!q.identity && !c.sel.empty()) {
+        std::vector<char> in_sel(n_side, 0);
+        for (int j : c.sel) in_sel[j] = 1;
+        for (int a = 0; a < n_side; ++a)
+            if (!in_sel[a])
+                for (int k = 0; k < q.ncols; ++k)
+                    if (q.hc[(size_t)a * q.ncols + k] != 0.0) return false;
+        return true;
+    }
+    return false;
+}
+
+// Solve every request in ONE batch (all their RHS iterate together) and cache them.
+void solve_and_cache(dot_problem* P, const std::vector<Req>& reqs) {
+    std::vector<Seg> segs;
+    std::vector<DBuf<double>> dcs;
+    int total = 0;
+    for (const Req& q : reqs) {
+        dcs.emplace_back();
+        if (!q.identity) dcs.back() = to_device(P, q.hc.data(), q.hc.size(), DOT_HOST);
+        segs.push_back(Seg{q.side, q.identity ? nullptr : dcs.back().get(), q.ncols});
+        total += P->n_freq * q.ncols;
+    }
+    const size_t nPp = (size_t)std::max(P->nP, 1);
+    DBuf<double2> XPj(P->arena, (size_t)total * nPp);
+    solve_batch(P, segs, total, nullptr, nullptr, XPj.get(), nullptr);
+    size_t off = 0;
+    for (const Req& q : reqs) {
+        const int n_side = q.side == 0 ? P->n_src : P->n_det;
+        FieldCache& c = P->cache[q.side];
+        c.valid = false;
+        c.X.reset();
+        const size_t n = (size_t)P->n_freq * q.ncols * nPp;
+        c.X = DBuf<double2>(P->arena, n);
+        DOT_CUDA_TRY(cudaMemcpyAsync(c.X.get(), XPj.get() + off, n * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                     P->stream));
+        off += n;
+        c.valid = true;
+        c.identity = q.identity;
+        c.ncols = q.ncols;
+        c.coeff = q.identity ? std::vector<double>() : q.hc;
+        c.sel.clear();
+        if (q.identity) {
+            for (int a = 0; a < n_side; ++a) c.sel.push_back(a);
+        } else {
+            // selection matrix? every column a unit vector e_a
+            bool is_sel = true;
+            std::vector<int> sel(q.ncols, -1);
+            for (int k = 0; k < q.ncols && is_sel; ++k)
+                for (int a = 0; a < n_side; ++a) {
+                    const double v = q.hc[(size_t)a * q.ncols + k];
+                    if (v == 0.0) continue;
+                    if (v != 1.0 || sel[k] >= 0) { is_sel = false; break; }
+                    sel[k] = a;
+                }
+            for (int k = 0; k < q.ncols && is_sel; ++k) is_sel = sel[k] >= 0;
+            if (is_sel) c.sel = sel;
+        }
+    }
+    sync(P);
+}
+
+// Before a call that needs the fields of several requests: solve all uncached ones
+// together (e.g. the forward W and adjoint V solves of dot_jacobian, L966).
+void prefetch_fields(dot_problem* P, const std::vector<Req>& reqs) {
+    std::vector<Req> miss;
+    for (const Req& q : reqs)
+        if (!cache_hit(P, q)) miss.push_back(q);
+    if (!miss.empty()) solve_and_cache(P, miss);
+}
+
 // Sampled fields for `side` and coefficients (host copy hc; empty = identity):
 // returns a pointer to [n_freq][ncols][nP]; `tmp` receives storage when the
 // fields are formed by combination rather than taken from the cache.
 const double2* get_fields(dot_problem* P, int side, const std::vector<double>& hc, bool identity, int ncols,
                           DBuf<double2>& tmp) {
-    const int n_side = side == 0 ? P->n_src : P->n_det;
+    const Req q{side, hc, identity, ncols};
+    if (!cache_hit(P, q)) solve_and_cache(P, {q});
     FieldCache& c = P->cache[side];
-    if (c.valid) {
-        if (identity && c.identity) return c.X.get();
-        if (!identity && !c.identity && c.ncols == ncols && c.coeff == hc) return c.X.get();
-        if (!identity && !c.sel.empty()) {
-            // The cache holds the fields of the point sources sel[0..m) (a selection /
-            // identity matrix).  If the request only combines those sources, form it by
-            // linear combination (no solves): X'[f][c][q] = sum_j coeff[sel_j][c] X[f][j][q].
-            const int m = (int)c.sel.size();
-            std::vector<char> in_sel(n_side, 0);
-            for (int j = 0; j < m; ++j) in_sel[c.sel[j]] = 1;
-            bool ok = true;
-            for (int a = 0; a < n_side && ok; ++a)
-                if (!in_sel[a])
-                    for (int q = 0; q < ncols; ++q)
-                        if (hc[(size_t)a * ncols + q] != 0.0) { ok = false; break; }
-            if (ok) {
-                std::vector<double> X((size_t)m * ncols);
-                for (int j = 0; j < m; ++j)
-                    for (int q = 0; q < ncols; ++q) X[(size_t)j * ncols + q] = hc[(size_t)c.sel[j] * ncols + q];
-                DBuf<double> dc = to_device(P, X.data(), X.size(), DOT_HOST);
-                tmp = DBuf<double2>(P->arena, (size_t)P->n_freq * ncols * std::max(P->nP, 1));
-                launch_rc_gemm(P->n_freq, ncols, P->nP, m, dc.get(), ncols, c.X.get(), (size_t)m * P->nP, P->nP, 1,
-                               tmp.get(), (size_t)ncols * P->nP, P->nP, 1, P->stream);
-                P->stats.kernel_launches++;
-                return tmp.get();
-            }
-        }
-    }
-    // solve and cache
-    c.valid = false;
-    c.X.reset();
-    c.X = DBuf<double2>(P->arena, (size_t)P->n_freq * ncols * std::max(P->nP, 1));
-    DBuf<double> dc;
-    if (!identity) dc = to_device(P, hc.data(), hc.size(), DOT_HOST);
-    solve_rhs(P, side, identity ? nullptr : dc.get(), ncols, P->n_freq * ncols, nullptr, nullptr, c.X.get(),
-              nullptr);
-    c.valid = true;
-    c.identity = identity;
-    c.ncols = ncols;
-    c.coeff = identity ? std::vector<double>() : hc;
-    c.sel.clear();
-    if (identity) {
-        for (int a = 0; a < n_side; ++a) c.sel.push_back(a);
-    } else {
-        // selection matrix? every column a unit vector e_a
-        bool is_sel = true;
-        std::vector<int> sel(ncols, -1);
-        for (int q = 0; q < ncols && is_sel; ++q)
-            for (int a = 0; a < n_side; ++a) {
-                const double v = hc[(size_t)a * ncols + q];
-                if (v == 0.0) continue;
-                if (v != 1.0 || sel[q] >= 0) { is_sel = false; break; }
-                sel[q] = a;
-            }
-        for (int q = 0; q < ncols && is_sel; ++q) is_sel = sel[q] >= 0;
-        if (is_sel) c.sel = sel;
-    }
-    return c.X.get();
+    if (identity && c.identity) return c.X.get();
+    if (!identity && !c.identity && c.ncols == ncols && c.coeff == hc) return c.X.get();
+    // combination of the cached point sources sel[0..m):
+    // X'[f][c][q] = sum_j coeff[sel_j][c] X[f][j][q]
+    const int m = (int)c.sel.size();
+    std::vector<double> X((size_t)m * ncols);
+    for (int j = 0; j < m; ++j)
+        for (int k = 0; k < ncols; ++k) X[(size_t)j * ncols + k] = hc[(size_t)c.sel[j] * ncols + k];
+    DBuf<double> dc = to_device(P, X.data(), X.size(), DOT_HOST);
+    tmp = DBuf<double2>(P->arena, (size_t)P->n_freq * ncols * std::max(P->nP, 1));
+    launch_rc_gemm(P->n_freq, ncols, P->nP, m, dc.get(), ncols, c.X.get(), (size_t)m * P->nP, P->nP, 1, tmp.get(),
+                   (size_t)ncols * P->nP, P->nP, 1, P->stream);
+    P->stats.kernel_launches++;
+    sync(P);
+    return tmp.get();
 }
 
 void invalidate_caches(dot_problem* P) {
@@ -676,6 +752,7 @@ int dot_jacobian(dot_problem* P, const double* W, int32_t ls, const double* V, i
     const int nf = P->n_freq, K = P->K;
     std::vector<double> hW = W ? host_copy(P, W, (size_t)P->n_src * ls, where) : std::vector<double>();
     std::vector<double> hV = V ? host_copy(P, V, (size_t)P->n_det * ld, where) : std::vector<double>();
+    prefetch_fields(P, {Req{0, hW, W == nullptr, ls}, Req{1, hV, V == nullptr, ld}});   // one joint batch
     DBuf<double2> tmpU, tmpL;
     const double2* XU = get_fields(P, 0, hW, W == nullptr, ls, tmpU);
     const double2* XL = get_fields(P, 1, hV, V == nullptr, ld, tmpL);
@@ -720,6 +797,7 @@ int dot_optimize_directions(dot_problem* P, int32_t k, const double* W, int32_t 
     if (k < 0 || k >= ls || k >= ld) throw Error(DOT_ERR_ARG, "need 0 <= k < min(ls, ld)");
     std::vector<double> hW = host_copy(P, W, (size_t)P->n_src * ls, where);
     std::vector<double> hV = host_copy(P, V, (size_t)P->n_det * ld, where);
+    prefetch_fields(P, {Req{0, {}, true, P->n_src}, Req{1, {}, true, P->n_det}});
     DBuf<double2> t0, t1;
     const double2* XU = get_fields(P, 0, {}, true, P->n_src, t0);
     const double2* XL = get_fields(P, 1, {}, true, P->n_det, t1);
