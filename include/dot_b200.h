@@ -52,6 +52,7 @@ extern "C" {
 #define DOT_DEVICE 1
 
 typedef struct dot_problem dot_problem;
+typedef struct dot_dd dot_dd;          /* z-slab domain-decomposition group */
 
 /* Problem description.  All pointers are HOST pointers, copied by dot_create. */
 typedef struct dot_config {
@@ -173,6 +174,33 @@ int dot_optimize_directions_subspace(dot_problem* P, int32_t k, int32_t iters, i
                                      int32_t ls, const double* V, int32_t ld, const double* X0_src,
                                      const double* X0_det, int where, double* W_out, double* V_out,
                                      double* objective_out);
+
+/* ---- z-slab domain decomposition (BASELINE north_star: "by z-slab domain decomposition
+ * with NCCL halo exchange and an allreduce of Krylov inner products in the few-
+ * simultaneous-source regime").  Rank r of `world`
+ * owns a contiguous range of z chunks and iterates only those planes (plus the halo
+ * planes it recomputes); after every COCG pass the two boundary planes of r_{k+1}
+ * and p_k go to the neighbours and the per-chunk partial sums of the Krylov inner
+ * products are all-reduced, so all ranks take identical steps.  Sampled solutions
+ * are all-reduced at the end and land in each rank's field caches, after which
+ * dot_misfit / dot_jacobian / dot_solve_sampled on any rank use them without solves.
+ *
+ * dot_nccl_unique_id: 128-byte NCCL id (host); rank 0 creates it, the caller
+ *   broadcasts it (e.g. torch.distributed).  NCCL is loaded at run time.
+ * dot_dd_create: `local` [nlocal] problems of ranks rank0 .. rank0+nlocal-1.  Either
+ *   nlocal == world (all ranks in this process, exchanged with device copies -- the
+ *   single-GPU emulation) or nlocal == 1 with nccl_id (one rank per process / GPU).
+ *   All ranks hold the same problem and parameters (dot_set_params on each).
+ * dot_dd_fields: solve the forward fields of B W (ls columns; W NULL = identity;
+ *   ls = 0: none) and the adjoint fields of C V (ld; likewise) for every frequency
+ *   in one decomposed batch and cache them on every local rank.  Errors as
+ *   dot_misfit; DOT_ERR_ARG if nz < 2 * world. */
+int dot_nccl_unique_id(unsigned char* id_out);
+int dot_dd_create(dot_problem* const* local, int32_t nlocal, int32_t rank0, int32_t world,
+                  const unsigned char* nccl_id, dot_dd** out);
+int dot_dd_fields(dot_dd* G, const double* W, int32_t ls, const double* V, int32_t ld, int where);
+const char* dot_dd_last_error(const dot_dd* G);
+int dot_dd_destroy(dot_dd* G);
 
 /* ---- component calls (same kernels; used by the parity tests) ---- */
 

@@ -2,6 +2,8 @@
 // and the paper-level calls set_params / misfit / jacobian / optimize_directions
 // (include/dot_b200.h documents every entry point).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -159,6 +161,26 @@ std::vector<int32_t> solve_rhs(dot_problem* P, int side, const double* d_coeff, 
     return solve_batch(P, segs, n_rhs, dense, d_freq_of, XP, Xfull);
 }
 
+// R0 [nb][N] and shift [nb] of global RHS r0 .. r0+nb-1 of the concatenated segments.
+void build_point_rhs(dot_problem* P, const std::vector<Seg>& segs, long long r0, int nb, double2* R0, double* shift) {
+    const size_t N = P->N;
+    DOT_CUDA_TRY(cudaMemsetAsync(R0, 0, (size_t)nb * N * sizeof(double2), P->stream));
+    long long gs = 0;
+    for (const Seg& sg : segs) {                 // the part of each segment inside [r0, r0 + nb)
+        const long long ge = gs + (long long)P->n_freq * sg.ncols;
+        const long long rs = std::max<long long>(r0, gs), re = std::min<long long>(r0 + nb, ge);
+        if (rs < re) {
+            const int nn = sg.side == 0 ? P->n_src : P->n_det;
+            launch_scatter_rhs(R0 + (size_t)(rs - r0) * N, N, (int)(re - rs), rs - gs, sg.ncols,
+                               sg.side == 0 ? P->d_src.get() : P->d_det.get(), nn, sg.d_coeff,
+                               sg.side == 0 ? P->d_src_scale.get() : P->d_det_scale.get(), P->stream);
+            launch_fill_shift(shift + (rs - r0), (int)(re - rs), rs - gs, sg.ncols, P->d_omega_nu.get(), P->stream);
+            P->stats.kernel_launches += 2;
+        }
+        gs = ge;
+    }
+}
+
 // Batched solve of the concatenated RHS lists of `segs` (point mode) or of the dense
 // vectors `dense` (with per-RHS frequency d_freq_of).  All RHS iterate together in
 // chunks of what fits the workspace.
@@ -205,22 +227,7 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, i
             DOT_CUDA_TRY(cudaMemcpyAsync(R0.get(), dense + (size_t)r0 * N, (size_t)nb * N * sizeof(double2),
                                          cudaMemcpyDeviceToDevice, P->stream));
         } else {
-            DOT_CUDA_TRY(cudaMemsetAsync(R0.get(), 0, (size_t)nb * N * sizeof(double2), P->stream));
-            long long gs = 0;
-            for (const Seg& sg : segs) {                 // the part of each segment inside [r0, r0 + nb)
-                const long long ge = gs + (long long)P->n_freq * sg.ncols;
-                const long long rs = std::max<long long>(r0, gs), re = std::min<long long>(r0 + nb, ge);
-                if (rs < re) {
-                    const int nn = sg.side == 0 ? P->n_src : P->n_det;
-                    launch_scatter_rhs(R0.get() + (size_t)(rs - r0) * N, N, (int)(re - rs), rs - gs, sg.ncols,
-                                       sg.side == 0 ? P->d_src.get() : P->d_det.get(), nn, sg.d_coeff,
-                                       sg.side == 0 ? P->d_src_scale.get() : P->d_det_scale.get(), P->stream);
-                    launch_fill_shift(shift.get() + (rs - r0), (int)(re - rs), rs - gs, sg.ncols,
-                                      P->d_omega_nu.get(), P->stream);
-                    P->stats.kernel_launches += 2;
-                }
-                gs = ge;
-            }
+            build_point_rhs(P, segs, r0, nb, R0.get(), shift.get());
         }
         if (d_freq_of) {
             // shift[r] = omega_nu[freq_of[r0 + r]] : reuse fill_shift with ncols = 1 on a gathered table
@@ -254,6 +261,8 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, i
         a.part[0] = part.get();
         a.part[1] = part.get() + (size_t)nb * P->tl.ntiles * nzch * kNumPartials;
         a.nzch = nzch;
+        a.nzch_tot = nzch;
+        a.zc0 = 0;
         a.zlen = (P->nz + nzch - 1) / nzch;
         a.st[0] = st.get();
         a.st[1] = st.get() + nb;
@@ -457,6 +466,315 @@ void check_side_matrix(const double* M, int n_side, int ncols, const char* name)
     if (!M && ncols != n_side) throw Error(DOT_ERR_ARG, std::string(name) + " = NULL (identity) needs ncols = n");
 }
 
+
+// ======================================================== z-slab domain decomposition
+// (BASELINE north_star: "by z-slab domain decomposition with NCCL halo exchange and an
+// allreduce of Krylov inner products in the few-simultaneous-source regime";
+// DESIGN.md "Domain decomposition").  Rank r owns the z chunks [cb[r], cb[r+1]) of a
+// global chunking (zlen planes per chunk) and runs the z pass on them; after every
+// pass the two boundary planes of r_{k+1} and p_k are exchanged with the neighbours
+// and the per-chunk partial sums (disjoint slots) are all-reduced, so every rank
+// derives the same Krylov scalars.  Sampled solutions are all-reduced at the end.
+// Ranks live either in one process (several dot_problem, exchanged with device
+// copies: the single-GPU emulation the tests use) or one per process with NCCL.
+
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+    decltype(&ncclCommInitRank) commInitRank = nullptr;
+    decltype(&ncclCommDestroy) commDestroy = nullptr;
+    decltype(&ncclSend) send = nullptr;
+    decltype(&ncclRecv) recv = nullptr;
+    decltype(&ncclAllReduce) allReduce = nullptr;
+    decltype(&ncclGroupStart) groupStart = nullptr;
+    decltype(&ncclGroupEnd) groupEnd = nullptr;
+    decltype(&ncclGetErrorString) errStr = nullptr;
+};
+
+// NCCL is loaded on first use (libnccl.so.2: the one torch already loaded, else the system one)
+NcclApi& nccl_api() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        api.why = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
+        return api;
+    }
+    bool ok = true;
+    auto sym = [&](const char* n) {
+        void* f = dlsym(h, n);
+        if (!f) ok = false;
+        return f;
+    };
+    api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(sym("ncclGetUniqueId"));
+    api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(sym("ncclCommInitRank"));
+    api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(sym("ncclCommDestroy"));
+    api.send = reinterpret_cast<decltype(api.send)>(sym("ncclSend"));
+    api.recv = reinterpret_cast<decltype(api.recv)>(sym("ncclRecv"));
+    api.allReduce = reinterpret_cast<decltype(api.allReduce)>(sym("ncclAllReduce"));
+    api.groupStart = reinterpret_cast<decltype(api.groupStart)>(sym("ncclGroupStart"));
+    api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(sym("ncclGroupEnd"));
+    api.errStr = reinterpret_cast<decltype(api.errStr)>(sym("ncclGetErrorString"));
+    api.ok = ok;
+    if (!ok) api.why = "libnccl.so.2 lacks a required symbol";
+    return api;
+}
+
+#define DOT_NCCL_TRY(expr)                                                                        \
+    do {                                                                                          \
+        ncclResult_t _r = (expr);                                                                 \
+        if (_r != ncclSuccess)                                                                    \
+            throw Error(DOT_ERR_CUDA, std::string(#expr) + ": " + nccl_api().errStr(_r));         \
+    } while (0)
+
+struct DDPlan {
+    int C = 1, zlen = 0;
+    std::vector<int> cb;            // chunk boundaries of the global ranks, size world + 1
+    int zs(int r, int nz) const { return std::min(cb[r] * zlen, nz); }
+    int ze(int r, int nz) const { return std::min(cb[r + 1] * zlen, nz); }
+};
+
+}  // namespace
+
+struct dot_dd {
+    std::vector<dot_problem*> loc;  // local ranks rank0 .. rank0 + loc.size() - 1
+    int rank0 = 0, world = 1;
+    ncclComm_t comm = nullptr;      // one local rank per process when set
+    std::string err;
+};
+
+namespace {
+
+DDPlan dd_plan(const dot_dd* G, int nb) {
+    const dot_problem* P = G->loc[0];
+    DDPlan pl;
+    const int W = G->world, nz = P->nz;
+    // chunks per rank from the fill target of one GPU (4 CTAs per SM), at least 2 planes each
+    const long long target = 4LL * P->num_sms, have = (long long)P->tl.ntiles * nb;
+    int m = have < target ? (int)((target + have - 1) / have) : 1;
+    int zlen = std::max(2, (nz + W * m - 1) / (W * m));
+    int C = (nz + zlen - 1) / zlen;
+    if (C < W) {
+        zlen = std::max(2, nz / W);
+        C = (nz + zlen - 1) / zlen;
+    }
+    if (C < W) throw Error(DOT_ERR_ARG, "z-slab decomposition: nz too small for this many ranks (need 2 planes per rank)");
+    pl.C = C;
+    pl.zlen = zlen;
+    pl.cb.resize(W + 1);
+    for (int r = 0; r <= W; ++r) pl.cb[r] = (int)((long long)r * C / W);
+    return pl;
+}
+
+// DD solve of the point-combination requests: fills the field caches of every local rank.
+void dd_solve(dot_dd* G, const std::vector<Req>& reqs) {
+    const int L = (int)G->loc.size();
+    dot_problem* P0 = G->loc[0];
+    const size_t N = P0->N, PS = (size_t)P0->nx * P0->ny;
+    const int nz = P0->nz, nP = P0->nP, nf = P0->n_freq;
+    int nb = 0;
+    for (const Req& q : reqs) nb += nf * q.ncols;
+    if (nb == 0) return;
+    const DDPlan pl = dd_plan(G, nb);
+    const int ntiles = P0->tl.ntiles, nslots = ntiles * pl.C;
+    const bool use_nccl = G->comm != nullptr;
+    if (P0->tl.kind != 1) throw Error(DOT_ERR_ARG, "domain decomposition needs the z pass (DOT_COCG_KERNEL != ring)");
+
+    struct RankBufs {
+        std::vector<DBuf<double>> dcs;
+        DBuf<double2> R[2], Pv[2], XP;
+        DBuf<double> part, shift;
+        DBuf<RhsState> st;
+        PassArgs a;
+    };
+    std::vector<RankBufs> B(L);
+    for (int q = 0; q < L; ++q) {
+        dot_problem* P = G->loc[q];
+        RankBufs& b = B[q];
+        std::vector<Seg> segs;
+        for (const Req& rq : reqs) {
+            b.dcs.emplace_back();
+            if (!rq.identity) b.dcs.back() = to_device(P, rq.hc.data(), rq.hc.size(), DOT_HOST);
+            segs.push_back(Seg{rq.side, rq.identity ? nullptr : b.dcs.back().get(), rq.ncols});
+        }
+        for (int i = 0; i < 2; ++i) {
+            b.R[i] = DBuf<double2>(P->arena, (size_t)nb * N);
+            b.Pv[i] = DBuf<double2>(P->arena, (size_t)nb * N);
+        }
+        b.XP = DBuf<double2>(P->arena, (size_t)nb * std::max(nP, 1));
+        b.part = DBuf<double>(P->arena, 2 * (size_t)nb * nslots * kNumPartials);
+        b.shift = DBuf<double>(P->arena, nb);
+        b.st = DBuf<RhsState>(P->arena, 2 * (size_t)nb);
+        build_point_rhs(P, segs, 0, nb, b.R[0].get(), b.shift.get());
+        DOT_CUDA_TRY(cudaMemsetAsync(b.XP.get(), 0, (size_t)nb * std::max(nP, 1) * sizeof(double2), P->stream));
+        DOT_CUDA_TRY(cudaMemsetAsync(b.part.get(), 0, 2 * (size_t)nb * nslots * kNumPartials * sizeof(double), P->stream));
+        PassArgs& a = b.a;
+        a.op = P->op;
+        a.tl = P->tl;
+        a.max_iter = P->max_iter;
+        a.tol2 = P->tol * P->tol;
+        a.mu = P->d_mu.get();
+        a.shift = b.shift.get();
+        for (int i = 0; i < 2; ++i) {
+            a.R[i] = b.R[i].get();
+            a.Pv[i] = b.Pv[i].get();
+            a.part[i] = b.part.get() + (size_t)i * nb * nslots * kNumPartials;
+            a.st[i] = b.st.get() + (size_t)i * nb;
+        }
+        a.samp_nodes = P->d_P.get();
+        a.samp_off = P->d_off.get();
+        a.XP = b.XP.get();
+        a.nP = nP;
+        a.X = nullptr;
+        const int r = G->rank0 + q;
+        a.zlen = pl.zlen;
+        a.nzch_tot = pl.C;
+        a.zc0 = pl.cb[r];
+        a.nzch = pl.cb[r + 1] - pl.cb[r];
+        launch_cocg_init(a, nb, P->stream);      // full-domain sums of b: identical on every rank
+        P->stats.kernel_launches += 1;
+    }
+    // boundary planes [z, z + n) of vector arrays V (nb vectors of N) : (dst rank q', src rank q)
+    auto copy_planes = [&](double2* dst, const double2* src, int z, int n, cudaStream_t s) {
+        if (n <= 0) return;
+        DOT_CUDA_TRY(cudaMemcpy2DAsync(dst + (size_t)z * PS, N * sizeof(double2), src + (size_t)z * PS,
+                                       N * sizeof(double2), (size_t)n * PS * sizeof(double2), nb,
+                                       cudaMemcpyDeviceToDevice, s));
+    };
+    const int CHK = 8;
+    int k = 0;
+    for (;;) {
+        const int kout = (k + 1) & 1;
+        for (int q = 0; q < L; ++q) {
+            dot_problem* P = G->loc[q];
+            PassArgs& a = B[q].a;
+            a.k = k;
+            if (use_nccl)   // this rank's slots only; the others arrive through the all-reduce
+                DOT_CUDA_TRY(cudaMemsetAsync(a.part[kout], 0, (size_t)nb * nslots * kNumPartials * sizeof(double),
+                                             P->stream));
+            launch_cocg_pass(a, nb, P->stream);
+            P->stats.kernel_launches++;
+            P->stats.pass_launches++;
+        }
+        // ---- halo exchange of r_{k+1}, p_k (kout arrays) and all-reduce of the partials
+        if (!use_nccl) {
+            for (int q = 0; q < L; ++q) DOT_CUDA_TRY(cudaStreamSynchronize(G->loc[q]->stream));
+            cudaStream_t s = G->loc[0]->stream;
+            for (int q = 0; q + 1 < L; ++q) {
+                const int r = G->rank0 + q;
+                const int zt = pl.ze(r, nz);                         // boundary between r and r + 1
+                for (int v = 0; v < 2; ++v) {
+                    double2* lo = v == 0 ? B[q].a.R[kout] : B[q].a.Pv[kout];
+                    double2* hi = v == 0 ? B[q + 1].a.R[kout] : B[q + 1].a.Pv[kout];
+                    copy_planes(hi, lo, std::max(zt - 2, pl.zs(r, nz)), std::min(2, zt - pl.zs(r, nz)), s);
+                    copy_planes(lo, hi, zt, std::min(zt + 2, pl.ze(r + 1, nz)) - zt, s);
+                }
+            }
+            for (int q = 0; q < L; ++q)            // owned slot ranges to every other local rank
+                for (int q2 = 0; q2 < L; ++q2) {
+                    if (q2 == q) continue;
+                    const int r = G->rank0 + q;
+                    const size_t off = (size_t)pl.cb[r] * ntiles * kNumPartials;
+                    const size_t w = (size_t)(pl.cb[r + 1] - pl.cb[r]) * ntiles * kNumPartials * sizeof(double);
+                    DOT_CUDA_TRY(cudaMemcpy2DAsync(B[q2].a.part[kout] + off, nslots * kNumPartials * sizeof(double),
+                                                   B[q].a.part[kout] + off, nslots * kNumPartials * sizeof(double),
+                                                   w, nb, cudaMemcpyDeviceToDevice, s));
+                }
+            DOT_CUDA_TRY(cudaStreamSynchronize(s));
+        } else {
+            NcclApi& nc = nccl_api();
+            dot_problem* P = G->loc[0];
+            const int r = G->rank0;
+            const int zs = pl.zs(r, nz), ze = pl.ze(r, nz);
+            DOT_NCCL_TRY(nc.groupStart());
+            for (int v = 0; v < 2; ++v) {
+                double2* X = v == 0 ? B[0].a.R[kout] : B[0].a.Pv[kout];
+                for (int i = 0; i < nb; ++i) {
+                    double2* Xi = X + (size_t)i * N;
+                    if (r + 1 < G->world) {                 // top planes up, halo from above
+                        const int n_up = std::min(2, ze - zs), n_dn = std::min(ze + 2, pl.ze(r + 1, nz)) - ze;
+                        DOT_NCCL_TRY(nc.send(Xi + (size_t)(ze - n_up) * PS, 2 * n_up * PS, ncclDouble, r + 1, G->comm,
+                                             P->stream));
+                        DOT_NCCL_TRY(nc.recv(Xi + (size_t)ze * PS, 2 * n_dn * PS, ncclDouble, r + 1, G->comm, P->stream));
+                    }
+                    if (r > 0) {                            // bottom planes down, halo from below
+                        const int n_dn = std::min(2, ze - zs), n_up = std::min(2, zs - pl.zs(r - 1, nz));
+                        DOT_NCCL_TRY(nc.send(Xi + (size_t)zs * PS, 2 * n_dn * PS, ncclDouble, r - 1, G->comm, P->stream));
+                        DOT_NCCL_TRY(nc.recv(Xi + (size_t)(zs - n_up) * PS, 2 * n_up * PS, ncclDouble, r - 1, G->comm,
+                                             P->stream));
+                    }
+                }
+            }
+            DOT_NCCL_TRY(nc.groupEnd());
+            DOT_NCCL_TRY(nc.allReduce(B[0].a.part[kout], B[0].a.part[kout], (size_t)nb * nslots * kNumPartials,
+                                      ncclDouble, ncclSum, G->comm, P->stream));
+        }
+        ++k;
+        if (k % CHK == 0 || k > P0->max_iter) {
+            dot_problem* P = G->loc[0];
+            launch_count_active(B[0].a.st[(k - 1) & 1], nb, P->d_count.get(), P->stream);
+            DOT_CUDA_TRY(cudaMemcpyAsync(P->h_count, P->d_count.get(), sizeof(int), cudaMemcpyDeviceToHost, P->stream));
+            sync(P);
+            if (*P->h_count == 0) break;
+        }
+    }
+    // ---- sampled solutions: each sample node belongs to one slab -> sum over ranks
+    const size_t nx = (size_t)nb * std::max(nP, 1);
+    if (!use_nccl) {
+        for (int q = 1; q < L; ++q) launch_cadd_inplace(B[0].XP.get(), B[q].XP.get(), nx, G->loc[0]->stream);
+        for (int q = 1; q < L; ++q)
+            DOT_CUDA_TRY(cudaMemcpyAsync(B[q].XP.get(), B[0].XP.get(), nx * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                         G->loc[0]->stream));
+        DOT_CUDA_TRY(cudaStreamSynchronize(G->loc[0]->stream));
+    } else {
+        DOT_NCCL_TRY(nccl_api().allReduce(B[0].XP.get(), B[0].XP.get(), 2 * nx, ncclDouble, ncclSum, G->comm,
+                                          G->loc[0]->stream));
+    }
+    // ---- convergence flags, statistics and the field caches of every local rank
+    for (int q = 0; q < L; ++q) {
+        dot_problem* P = G->loc[q];
+        std::vector<RhsState> hs(nb);
+        DOT_CUDA_TRY(cudaMemcpyAsync(hs.data(), B[q].a.st[(k - 1) & 1], nb * sizeof(RhsState), cudaMemcpyDeviceToHost,
+                                     P->stream));
+        sync(P);
+        int mx = 0, mn = 1 << 30;
+        for (int i = 0; i < nb; ++i) {
+            if (hs[i].flag == DOT_ERR_NOCONV) throw Error(DOT_ERR_NOCONV, "COCG (domain decomposition) did not converge");
+            if (hs[i].flag == DOT_ERR_BREAKDOWN) throw Error(DOT_ERR_BREAKDOWN, "COCG (domain decomposition) breakdown");
+            mx = std::max(mx, hs[i].iters);
+            mn = std::min(mn, hs[i].iters);
+            P->stats.rhs_iterations += hs[i].iters;
+            P->stats.pass_bytes += 64.0 * (double)N * hs[i].iters / G->world;
+        }
+        P->stats.rhs_solved += nb;
+        P->stats.last_max_iters = mx;
+        P->stats.last_min_iters = mn;
+        size_t off = 0;
+        const size_t nPp = (size_t)std::max(nP, 1);
+        for (const Req& rq : reqs) {
+            const int n_side = rq.side == 0 ? P->n_src : P->n_det;
+            FieldCache& c = P->cache[rq.side];
+            c.valid = false;
+            c.X.reset();
+            const size_t n = (size_t)nf * rq.ncols * nPp;
+            c.X = DBuf<double2>(P->arena, n);
+            DOT_CUDA_TRY(cudaMemcpyAsync(c.X.get(), B[q].XP.get() + off, n * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                         P->stream));
+            off += n;
+            c.valid = true;
+            c.identity = rq.identity;
+            c.ncols = rq.ncols;
+            c.coeff = rq.identity ? std::vector<double>() : rq.hc;
+            c.sel.clear();
+            if (rq.identity)
+                for (int a2 = 0; a2 < n_side; ++a2) c.sel.push_back(a2);
+        }
+        sync(P);
+    }
+}
 }  // namespace
 
 // ===================================================================== C ABI
@@ -1002,6 +1320,98 @@ int dot_fields_on_support(dot_problem* P, int32_t side, const double* coeff, int
     }
     sync(P);
     DOT_API_END(P)
+}
+
+int dot_nccl_unique_id(unsigned char* out) {
+    try {
+        if (!out) throw Error(DOT_ERR_ARG, "null argument");
+        NcclApi& nc = nccl_api();
+        if (!nc.ok) throw Error(DOT_ERR_CUDA, nc.why);
+        ncclUniqueId id;
+        DOT_NCCL_TRY(nc.getUniqueId(&id));
+        std::memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
+        return DOT_OK;
+    } catch (const Error& e) {
+        g_create_error = e.msg;
+        return e.code;
+    }
+}
+
+int dot_dd_create(dot_problem* const* local, int32_t nlocal, int32_t rank0, int32_t world,
+                  const unsigned char* nccl_id, dot_dd** out) {
+    std::unique_ptr<dot_dd> G;
+    try {
+        if (!local || !out || nlocal < 1 || world < 1 || rank0 < 0 || rank0 + nlocal > world)
+            throw Error(DOT_ERR_ARG, "bad rank layout");
+        if (nlocal < world && nlocal != 1)
+            throw Error(DOT_ERR_ARG, "either all ranks in this process or one rank per process");
+        G.reset(new dot_dd());
+        for (int q = 0; q < nlocal; ++q) {
+            if (!local[q]) throw Error(DOT_ERR_ARG, "null problem");
+            const dot_problem* A = local[0];
+            const dot_problem* Bq = local[q];
+            if (Bq->nx != A->nx || Bq->ny != A->ny || Bq->nz != A->nz || Bq->n_src != A->n_src ||
+                Bq->n_det != A->n_det || Bq->n_freq != A->n_freq || Bq->tl.TY != A->tl.TY)
+                throw Error(DOT_ERR_ARG, "ranks must hold the same problem");
+            G->loc.push_back(local[q]);
+        }
+        G->rank0 = rank0;
+        G->world = world;
+        if (nlocal < world) {
+            if (!nccl_id) throw Error(DOT_ERR_ARG, "multi-process decomposition needs an NCCL unique id");
+            NcclApi& nc = nccl_api();
+            if (!nc.ok) throw Error(DOT_ERR_CUDA, nc.why);
+            ncclUniqueId id;
+            std::memcpy(id.internal, nccl_id, NCCL_UNIQUE_ID_BYTES);
+            DOT_NCCL_TRY(nc.commInitRank(&G->comm, world, id, rank0));
+        }
+        *out = G.release();
+        return DOT_OK;
+    } catch (const Error& e) {
+        g_create_error = e.msg;
+        return e.code;
+    }
+}
+
+int dot_dd_destroy(dot_dd* G) {
+    if (!G) return DOT_OK;
+    if (G->comm) nccl_api().commDestroy(G->comm);
+    delete G;
+    return DOT_OK;
+}
+
+const char* dot_dd_last_error(const dot_dd* G) { return G ? G->err.c_str() : g_create_error.c_str(); }
+
+int dot_dd_fields(dot_dd* G, const double* W, int32_t ls, const double* V, int32_t ld, int where) {
+    if (!G) return DOT_ERR_ARG;
+    try {
+        dot_problem* P = G->loc[0];
+        for (dot_problem* Q : G->loc) require_params(Q);
+        std::vector<Req> reqs;
+        if (ls > 0) {
+            check_side_matrix(W, P->n_src, ls, "W");
+            reqs.push_back(Req{0, W ? host_copy(P, W, (size_t)P->n_src * ls, where) : std::vector<double>(),
+                               W == nullptr, ls});
+        }
+        if (ld > 0) {
+            check_side_matrix(V, P->n_det, ld, "V");
+            reqs.push_back(Req{1, V ? host_copy(P, V, (size_t)P->n_det * ld, where) : std::vector<double>(),
+                               V == nullptr, ld});
+        }
+        for (dot_problem* Q : G->loc)
+            for (auto& c : Q->cache) {
+                c.valid = false;
+                c.X.reset();
+            }
+        dd_solve(G, reqs);
+        return DOT_OK;
+    } catch (const Error& e) {
+        G->err = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        G->err = e.what();
+        return DOT_ERR_ARG;
+    }
 }
 
 int dot_contract(void* stream, int32_t nb, int32_t K, int32_t ld, int32_t ls, int32_t n_p, const double* Lam,

@@ -424,9 +424,9 @@ __global__ void __launch_bounds__(256) cocg_init_kernel(const PassArgs a) {
     block_reduce_partials(acc, scratch);
     if (threadIdx.x == 0) {
         // slot tile of z chunk 0 carries the sums; the slots of the other z chunks are zero
-        double* out = a.part[0] + ((size_t)rhs * a.tl.ntiles * a.nzch + tile) * kNumPartials;
+        double* out = a.part[0] + ((size_t)rhs * a.tl.ntiles * a.nzch_tot + tile) * kNumPartials;
         for (int i = 0; i < kNumPartials; ++i) out[i] = acc[i];
-        for (int zc = 1; zc < a.nzch; ++zc)
+        for (int zc = 1; zc < a.nzch_tot; ++zc)
             for (int i = 0; i < kNumPartials; ++i) out[(size_t)zc * a.tl.ntiles * kNumPartials + i] = 0.0;
     }
     if (threadIdx.x == 0 && tile == 0) {

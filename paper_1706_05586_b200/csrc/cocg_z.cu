@@ -47,7 +47,7 @@ struct ZScalars {
 // tiles, fixed-order butterfly reduction: identical in every CTA of the RHS).
 __device__ void zpass_scalars(const PassArgs& a, int rhs, int tile, ZScalars* out) {
     const int lane = threadIdx.x & 31;
-    const int ntiles = a.tl.ntiles * a.nzch;          // partial slots per RHS (tiles x z chunks)
+    const int ntiles = a.tl.ntiles * a.nzch_tot;      // partial slots per RHS (tiles x global z chunks)
     const double* pp = a.part[a.k & 1] + (size_t)rhs * ntiles * kNumPartials;
     double s[kNumPartials];
 #pragma unroll
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
     constexpr int LPD = 4;                              // L2 prefetch distance (planes)
     constexpr int PD = NS - 2;                          // TMA planes in flight
     const int ntiles = a.tl.ntiles;
-    const int tile = blockIdx.x % ntiles, zc = blockIdx.x / ntiles, rhs = blockIdx.y;
+    const int tile = blockIdx.x % ntiles, zc = a.zc0 + blockIdx.x / ntiles, rhs = blockIdx.y;
     const int nx = a.op.nx, ny = a.op.ny, nz = a.op.nz;
     const int TY = a.tl.TY;
     // z chunk [z0, z1) of this CTA; phase 1 runs on [a1, b1), phase 2 on [a2, b2)
@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
     if (threadIdx.x < kNumPartials) {
         double sum = 0;
         for (int w = 0; w < nw; ++w) sum += scratch[w * kNumPartials + threadIdx.x];
-        a.part[kout][((size_t)rhs * ntiles * a.nzch + blockIdx.x) * kNumPartials + threadIdx.x] = sum;
+        a.part[kout][((size_t)rhs * ntiles * a.nzch_tot + (size_t)zc * ntiles + tile) * kNumPartials + threadIdx.x] = sum;
     }
 }
 
@@ -458,7 +458,7 @@ template <bool FX, int MAXT, int MINB, int NS, int RPT>
 void launch_z_ns(const PassArgs& a, int nb, cudaStream_t s) {
     // mu rides in the bulk-copy group when every copy is 16-byte sized and aligned
     const bool mut = (a.op.nx % 2 == 0);
-    const bool zc = a.nzch > 1;
+    const bool zc = a.nzch > 1 || a.nzch_tot > 1;
     auto k = mut ? (zc ? cocg_zpass_kernel<FX, MAXT, MINB, NS, true, RPT, true>
                        : cocg_zpass_kernel<FX, MAXT, MINB, NS, true, RPT, false>)
                  : (zc ? cocg_zpass_kernel<FX, MAXT, MINB, NS, false, RPT, true>

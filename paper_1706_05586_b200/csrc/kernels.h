@@ -28,8 +28,10 @@ struct PassArgs {
     OpConst op;
     CocgTiling tl;
     int k = 0;                    // pass index
-    int nzch = 1;                 // z chunks per (tile, RHS) (z pass only; partial slots = ntiles * nzch)
+    int nzch = 1;                 // z chunks launched per (tile, RHS) (z pass only)
     int zlen = 0;                 // planes per z chunk
+    int zc0 = 0;                  // first (global) z chunk of this launch (z-slab domain decomposition)
+    int nzch_tot = 1;             // global z chunks: partial slots per RHS = ntiles * nzch_tot
     int max_iter = 0;
     double tol2 = 0;              // tol^2
     const double* mu = nullptr;   // [N] absorption
@@ -122,6 +124,8 @@ void launch_gather_cols(int nb, int rows, int ncols, const double2* X, size_t xb
                         const int32_t* idx, double2* out, size_t ob, size_t orow, cudaStream_t s);
 // a[i] -= b[i] (complex)
 void launch_csub_inplace(double2* a, const double2* b, size_t n, cudaStream_t s);
+// a[i] += b[i] (complex)
+void launch_cadd_inplace(double2* a, const double2* b, size_t n, cudaStream_t s);
 // *out = sum |a[i]|^2 (deterministic, single launch)
 void launch_sumsq(const double2* a, size_t n, double* out, cudaStream_t s);
 // Dt[f][s][d] = D[f][d][s]

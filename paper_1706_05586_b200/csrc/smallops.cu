@@ -43,6 +43,11 @@ __global__ void csub_kernel(double2* a, const double2* b, size_t n) {
         a[i] = csub(a[i], b[i]);
 }
 
+__global__ void cadd_kernel(double2* a, const double2* b, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        a[i] = cadd(a[i], b[i]);
+}
+
 __global__ void sumsq_kernel(const double2* a, size_t n, double* out) {
     __shared__ double ws[32];
     double s = 0.0;
@@ -123,6 +128,12 @@ void launch_gather_cols(int nb, int rows, int ncols, const double2* X, size_t xb
 void launch_csub_inplace(double2* a, const double2* b, size_t n, cudaStream_t s) {
     if (n == 0) return;
     csub_kernel<<<blocks_for(n), 256, 0, s>>>(a, b, n);
+    DOT_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_cadd_inplace(double2* a, const double2* b, size_t n, cudaStream_t s) {
+    if (!n) return;
+    cadd_kernel<<<blocks_for(n), 256, 0, s>>>(a, b, n);
     DOT_CUDA_TRY(cudaGetLastError());
 }
 

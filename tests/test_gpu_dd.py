@@ -1,0 +1,101 @@
+"""z-slab domain decomposition (north_star "z-slab domain decomposition with NCCL halo
+exchange and an allreduce of Krylov inner products"; DESIGN.md "Domain
+decomposition"), run with all ranks in one process on one GPU: every rank is a
+separate problem that iterates only its slab, and the halo planes / partial sums
+travel by device copies between passes (no kernel waits on another).  The results
+must match the oracle and the undecomposed solve."""
+import numpy as np
+import pytest
+
+from oracle import jacobian, measurements, misfit
+from tests._small import small_config, small_problem
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dot():
+    from paper_1706_05586_b200 import build
+    build.build()
+    import paper_1706_05586_b200 as d
+    return d
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300)
+
+
+CASES = [dict(n=(24, 20, 19), L=(4.0, 3.5, 3.0), src=(3, 2), det=(2, 3)),
+         dict(n=(16, 16, 16), L=(4.0, 4.0, 4.0), src=(4, 4), det=(4, 4))]
+
+
+@pytest.mark.parametrize("ci", range(len(CASES)))
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_local_dd_matches_oracle_and_undecomposed(dot, ci, world):
+    from paper_1706_05586_b200.dd import LocalDD
+    cfg = small_config(**CASES[ci], eps=0.4)
+    prob, wl = small_problem(cfg, with_data=True)
+    rng = np.random.default_rng(world)
+    W = np.sign(rng.standard_normal((cfg.n_s, 3)))
+    V = np.sign(rng.standard_normal((cfg.n_d, 2)))
+    ranks = []
+    for _ in range(world):
+        g = dot.DOTProblem.from_config(cfg, wl.src_nodes, wl.det_nodes)
+        g.set_data(prob.data)
+        g.set_params(wl.p)
+        g.reset_stats()
+        ranks.append(g)
+    dd = LocalDD(ranks)
+    dd.fields(W, V)
+    ref = dot.DOTProblem.from_config(cfg, wl.src_nodes, wl.det_nodes)
+    ref.set_data(prob.data)
+    ref.set_params(wl.p)
+    m_ref, J_ref = ref.misfit(W, V), ref.jacobian(W, V)
+    m_or, J_or = misfit(prob, wl.p, W, V), jacobian(prob, wl.p, W, V)
+    nf = len(cfg.freqs_hz)
+    for g in ranks:
+        st = g.stats()
+        assert st["rhs_solved"] == nf * (3 + 2)           # the decomposed batch only
+        m, J = g.misfit(W, V), g.jacobian(W, V)
+        assert g.stats()["rhs_solved"] == nf * (3 + 2)    # misfit / jacobian served from the caches
+        assert abs(m - m_ref) <= 1e-10 * m_ref
+        assert rel(J, J_ref) <= 1e-10
+        assert abs(m - m_or) <= 1e-8 * m_or
+        assert rel(J, J_or) <= 1e-7
+    dd.close()
+
+
+def test_local_dd_identity_fields_give_measurements(dot):
+    from paper_1706_05586_b200.dd import LocalDD
+    cfg = small_config(**CASES[0], eps=0.4)
+    prob, wl = small_problem(cfg, with_data=False)
+    ranks = []
+    for _ in range(3):
+        g = dot.DOTProblem.from_config(cfg, wl.src_nodes, wl.det_nodes)
+        g.set_params(wl.p)
+        ranks.append(g)
+    dd = LocalDD(ranks)
+    dd.fields(None, None, ld=0)                         # all point sources, no adjoint
+    Mref = measurements(prob, wl.p)
+    for g in ranks:
+        X = g.solve_sampled(0)
+        samp = g.samples()
+        M = np.transpose(X[:, :, np.searchsorted(samp, wl.det_nodes)], (0, 2, 1))
+        assert rel(M, Mref) < 1e-8
+    dd.close()
+
+
+def test_dd_rejects_too_many_ranks(dot):
+    from paper_1706_05586_b200 import DotError
+    from paper_1706_05586_b200.dd import LocalDD
+    cfg = small_config(n=(8, 8, 5), eps=0.4)
+    prob, wl = small_problem(cfg, with_data=False)
+    ranks = []
+    for _ in range(3):
+        g = dot.DOTProblem.from_config(cfg, wl.src_nodes, wl.det_nodes)
+        g.set_params(wl.p)
+        ranks.append(g)
+    dd = LocalDD(ranks)
+    with pytest.raises(DotError):
+        dd.fields(None, None)
+    dd.close()
