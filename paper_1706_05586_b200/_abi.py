@@ -5,7 +5,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libdot_b200.so")
+LIB_PATH = os.environ.get("DOT_LIB_PATH") or os.path.join(_HERE, "lib", "libdot_b200.so")
 
 DOT_OK, DOT_ERR_ARG, DOT_ERR_CUDA, DOT_ERR_STATE, DOT_ERR_NOCONV, DOT_ERR_WORKSPACE, DOT_ERR_BREAKDOWN = range(7)
 DOT_HOST, DOT_DEVICE = 0, 1

@@ -6,7 +6,7 @@
 #include <string>
 #include <vector>
 
-#include "../../include/dot_b200.h"
+#include "dot_b200.h"   // -I include
 
 #define DOT_CUDA_TRY(expr)                                                            \
     do {                                                                              \
