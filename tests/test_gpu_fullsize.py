@@ -110,3 +110,34 @@ def test_full64_sketched_jacobian_is_combination_of_full(full):
     Js = g.jacobian(wl.W, wl.V)
     ref = np.einsum("sl,dm,fdsk->fmlk", wl.W, wl.V, Jf)
     assert np.linalg.norm(Js - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+def test_all128_point_solves_true_residual_and_sampled():
+    """configs[4] grid (128^3, 1024 x 1024, 5 frequencies, 160 parameters): the z pass
+    at nx = 128 (tile height 4, 32 tiles) -- dense solves against the oracle operator's
+    true residual and the sampled batched solve of the same point sources."""
+    from paper_1706_05586_b200 import build
+    build.build()
+    import paper_1706_05586_b200 as dot
+    cfg = config_by_name("all128")
+    wl = make_workload(cfg)
+    g = dot.DOTProblem.from_config(cfg, wl.src_nodes, wl.det_nodes, max_rhs=64)
+    g.set_params(wl.p)
+    grid = make_grid(cfg.n, cfg.L)
+    from oracle import assemble
+    mu = absorption(wl.p, grid, cfg)
+    cols = [0, 517, 1023]
+    E = np.zeros((cfg.n_s, len(cols)))
+    E[cols, np.arange(len(cols))] = 1.0
+    Xs = g.solve_sampled(0, E)                      # [f][3][P]
+    samp = g.samples()
+    scale = grid.theta[wl.src_nodes] / grid.cell_volume
+    for f in (0, 4):
+        A = assemble(grid, cfg.D, mu, 2 * np.pi * cfg.freqs_hz[f], cfg.nu).tocsr()
+        b = np.zeros((len(cols), grid.N), complex)
+        for r, c in enumerate(cols):
+            b[r, wl.src_nodes[c]] = scale[c]
+        x, _ = g.solve(b, f)
+        for r in range(len(cols)):
+            assert np.linalg.norm(b[r] - A @ x[r]) / np.linalg.norm(b[r]) < 1e-14
+            assert np.abs(Xs[f, r] - x[r][samp]).max() <= 1e-10 * np.abs(x[r][samp]).max()
