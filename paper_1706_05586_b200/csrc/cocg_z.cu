@@ -261,6 +261,13 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
         any2 |= ph2[j];
         any_own |= own[j];
     }
+    bool all_in = true, all2 = true, all_own = true;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+        all_in &= indom[j];
+        all2 &= ph2[j];
+        all_own &= own[j];
+    }
     const int o = r0 * nx + x;                         // slot element of row 0
     const int o3 = o - nx;                             // Rbuf element of row 0
     const int go = (j0 - 2 + r0) * nx + x;             // plane offset of row 0 (may be outside; unused then)
@@ -319,17 +326,22 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
             if (any_in) {
                 double2* sr = slots + sl * slotW + o;
                 const double2 beta = sh_sc.beta;
+                auto p1 = [&](auto ALL) {
+                    constexpr bool A = decltype(ALL)::v != 0;
 #pragma unroll
-                for (int j = 0; j < RPT; ++j) {
-                    if (!indom[j]) continue;
-                    const double2 rf = sr[j * nx];
-                    pf[j] = first ? rf : cfma(beta, sr[slotE + j * nx], rf);
-                    sr[slotE + j * nx] = pf[j];
-                    if (own[j] && ownf) {
-                        pP[j * nx] = pf[j];
-                        if (FULLX) pX[j * nx] = cfma(sh_sc.alpha, pf[j], pX[j * nx]);
+                    for (int j = 0; j < RPT; ++j) {
+                        if (!A && !indom[j]) continue;
+                        const double2 rf = sr[j * nx];
+                        pf[j] = first ? rf : cfma(beta, sr[slotE + j * nx], rf);
+                        sr[slotE + j * nx] = pf[j];
+                        if (own[j] && ownf) {
+                            pP[j * nx] = pf[j];
+                            if (FULLX) pX[j * nx] = cfma(sh_sc.alpha, pf[j], pX[j * nx]);
+                        }
                     }
-                }
+                };
+                if (all_in) p1(IC<1>());
+                else p1(IC<0>());
             }
         }
         // ---- phase 2: plane g = f - 1
@@ -349,9 +361,11 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
                 const bool interior = g > 0 && g < nz - 1;
                 const PlaneCoef ce = interior ? PlaneCoef{} : plane_coef(a.op, g, shift);
                 const double2 alpha = sh_sc.alpha;
+                auto p2 = [&](auto ALL) {
+                constexpr bool A = decltype(ALL)::v != 0;
 #pragma unroll
                 for (int j = 0; j < RPT; ++j) {
-                    if (!ph2[j]) continue;
+                    if (!A && !ph2[j]) continue;
                     const int oj = o + j * nx;
                     const double2 xw = hasW ? sp[oj - 1] : z2;
                     const double2 xe = hasE ? sp[oj + 1] : z2;
@@ -373,6 +387,9 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
                         acc[7] = fma(pc.x, qv.y, fma(pc.y, qv.x, acc[7]));
                     }
                 }
+                };
+                if (all2) p2(IC<1>());
+                else p2(IC<0>());
             }
             if (!FULLX && a.nP > 0 && owng) {
                 const int2 sr2 = s_samp[g];
