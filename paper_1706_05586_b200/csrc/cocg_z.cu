@@ -179,9 +179,26 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
     __shared__ ZScalars sh_sc;
 
     if (threadIdx.x < 32) zpass_scalars(a, rhs, blockIdx.x, &sh_sc);
-    {   // zero the slot ring and Rbuf: rows outside the domain stay zero (Dirichlet y faces)
-        const int tot = NS * slotW + 3 * rbE;
-        for (int i = threadIdx.x; i < tot; i += blockDim.x) slots[i] = cmk(0, 0);
+    {   // rows outside the domain (edge tiles only) must read as zero (Dirichlet y faces):
+        // the p rows of every ring slot outside [rlo, rhi) and the Rbuf rows outside
+        // [rlo - 1, rhi - 1); nothing else is read before it is written
+        const int rlo_ = max(0, 2 - j0), rhi_ = min(TY + 4, ny - j0 + 2);
+        const int nlo = rlo_ * nx, nhi = (TY + 4 - rhi_) * nx;
+        if (nlo + nhi > 0) {
+            const int per = nlo + nhi;
+            for (int i = threadIdx.x; i < NS * per; i += blockDim.x) {
+                const int q = i / per, e = i - q * per;
+                const int el = e < nlo ? e : rhi_ * nx + (e - nlo);
+                slots[(size_t)q * slotW + slotE + el] = cmk(0, 0);
+            }
+            const int blo = max(0, rlo_ - 1) * nx, bhi_r = max(0, rhi_ - 1);
+            const int bper = blo + (TY + 2 - min(TY + 2, bhi_r)) * nx;
+            for (int i = threadIdx.x; i < 3 * bper; i += blockDim.x) {
+                const int q = i / bper, e = i - q * bper;
+                const int el = e < blo ? e : min(TY + 2, bhi_r) * nx + (e - blo);
+                rbuf[(size_t)q * rbE + el] = cmk(0, 0);
+            }
+        }
         if (!FULLX && a.nP > 0)
             for (int g = threadIdx.x; g < nz; g += blockDim.x)
                 s_samp[g] = make_int2(a.samp_off[g * ntiles + tile], a.samp_off[g * ntiles + tile + 1]);
