@@ -196,8 +196,8 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, i
     if (fit < 1) throw Error(DOT_ERR_WORKSPACE, "workspace too small for one right-hand side");
     const int chunk = (int)std::min<size_t>(fit, (size_t)n_rhs);
     const int CHK = 8;
-    // z chunks (z pass): enough CTAs to fill the GPU when few RHS iterate together
-    // (DESIGN.md "z chunks"); at least 8 planes per chunk.  DOT_COCG_ZCHUNKS overrides.
+    // z chunks (z pass): enough CTAs to fill the GPU when few RHS iterate together on a
+    // deep grid; at least 8 planes per chunk.  DOT_COCG_ZCHUNKS overrides.
     auto zchunks = [&](int nb) {
         if (P->tl.kind != 1) return 1;
         int n = 1;
@@ -205,9 +205,12 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, i
         if (e) {
             n = std::min(std::max(1, std::atoi(e)), std::max(1, P->nz / 4));
         } else {
+            // measured (tools/rowsweep.sh): chunks pay off on deep grids (opt96, 96^3: 94 -> 110
+            // RHS solves/s) but not on shallow ones, where a chunk's halo planes and CTA start-up
+            // dominate (sketch32, 32^3: 4 chunks 3720 vs none 4180)
             const long long target = 4LL * P->num_sms;
             const long long have = (long long)P->tl.ntiles * nb;
-            if (have < target) n = (int)((target + have - 1) / have);
+            if (have < target && P->nz >= 64) n = (int)((target + have - 1) / have);
             n = std::min(n, std::max(1, P->nz / 8));
         }
         const int zlen = (P->nz + n - 1) / n;
