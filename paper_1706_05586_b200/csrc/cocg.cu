@@ -552,7 +552,7 @@ CocgTiling cocg_tiling(int nx, int ny, int nz, int prefetch, size_t max_smem, in
                        int want_ty) {
     if (kind != 0) {
         CocgTiling t;
-        if (z_tiling(nx, ny, nz, std::max(1, std::min(prefetch, 2)), want_ty, t)) return t;
+        if (z_tiling(nx, ny, nz, std::max(1, std::min(prefetch, 3)), want_ty, t)) return t;
         if (kind == 1 && want_ty > 0) throw Error(DOT_ERR_ARG, "requested z-pass tile height does not fit");
     }
     return ring_tiling(nx, ny, nz, std::max(1, prefetch - (kind != 0 ? 1 : 0)), max_smem, max_threads);

@@ -150,7 +150,6 @@ __device__ __forceinline__ double2 stencil_int(const OpConst& op, double shift, 
 template <bool FULLX, int MAXT, int MINB, int NS, bool MUT, int RPT, bool ZC>
 __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    constexpr int LPD = 4;                              // L2 prefetch distance (planes)
     constexpr int PD = NS - 2;                          // TMA planes in flight
     const int ntiles = a.tl.ntiles;
     const int tile = blockIdx.x % ntiles, zc = a.zc0 + blockIdx.x / ntiles, rhs = blockIdx.y;
@@ -251,16 +250,8 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
                 "l"(a.mu + g), "r"(mu_bytes), "r"(bar)
                 : "memory");
     };
-    auto prefetch_l2 = [&](int z) {
-        const size_t g = (size_t)z * PS + tile_off;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Rin + g), "r"(tile_bytes) : "memory");
-        if (!first)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Pin + g), "r"(tile_bytes) : "memory");
-    };
     if (threadIdx.x == 0)
         for (int z = a1; z < a1 + PD && z < b1; ++z) issue(z, z - a1);
-    if (threadIdx.x == 32)
-        for (int z = a1 + PD; z < a1 + PD + LPD && z < b1; ++z) prefetch_l2(z);
 
     // ---- per-thread geometry: rows r0 .. r0 + RPT - 1 of column x
     const int t = threadIdx.x;
@@ -322,7 +313,6 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
         constexpr int i1 = (i0 + 2) % 3;               // (f - 1) % 3
         constexpr int i2 = (i0 + 1) % 3;               // (f - 2) % 3
         if (threadIdx.x == 0 && f + PD < b1) issue(f + PD, sl_iss);
-        if (threadIdx.x == 32 && f + PD + LPD < b1) prefetch_l2(f + PD + LPD);
         const bool ownf = !ZC || (f >= z0 && f < z1);
         if (!MUT && f < b1)
 #pragma unroll
@@ -512,7 +502,8 @@ void launch_z(const PassArgs& a, int nb, cudaStream_t s) {
     switch (a.tl.nslots) {
         case 3: launch_z_ns<FX, MAXT, MINB, 3, RPT>(a, nb, s); break;
         case 4: launch_z_ns<FX, MAXT, MINB, 4, RPT>(a, nb, s); break;
-        default: throw Error(DOT_ERR_ARG, "z pass supports 3..4 ring slots (DOT_COCG_PREFETCH 1..2)");
+        case 5: launch_z_ns<FX, MAXT, MINB, 5, RPT>(a, nb, s); break;
+        default: throw Error(DOT_ERR_ARG, "z pass supports 3..5 ring slots (DOT_COCG_PREFETCH 1..3)");
     }
 }
 
