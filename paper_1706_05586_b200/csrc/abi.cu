@@ -224,6 +224,8 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, i
         DBuf<double> part(P->arena, 2 * (size_t)nb * P->tl.ntiles * nzch * kNumPartials);
         DBuf<RhsState> st(P->arena, 2 * (size_t)nb);
         DBuf<double> shift(P->arena, nb);
+        DBuf<int32_t> act(P->arena, nb);                 // active-RHS list of the tail passes
+        int nb_launch = nb;
 
         // ---- right-hand sides
         if (dense) {
@@ -282,18 +284,23 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, i
         for (;;) {
             if (P->timing && k % CHK == 0) DOT_CUDA_TRY(cudaEventRecord(event_at(P, ev++), P->stream));
             a.k = k;
-            launch_cocg_pass(a, nb, P->stream);
+            launch_cocg_pass(a, nb_launch, P->stream);
             P->stats.kernel_launches++;
             P->stats.pass_launches++;
             ++k;
             if (k % CHK == 0 || k > P->max_iter) {
                 if (P->timing) DOT_CUDA_TRY(cudaEventRecord(event_at(P, ev++), P->stream));
-                launch_count_active(a.st[(k - 1) & 1], nb, P->d_count.get(), P->stream);
+                launch_count_active(a.st[(k - 1) & 1], nb, P->d_count.get(), P->stream,
+                                    P->tl.kind == 1 ? act.get() : nullptr);
                 P->stats.kernel_launches++;
                 DOT_CUDA_TRY(cudaMemcpyAsync(P->h_count, P->d_count.get(), sizeof(int), cudaMemcpyDeviceToHost,
                                              P->stream));
                 sync(P);
                 if (*P->h_count == 0) break;
+                if (P->tl.kind == 1) {     // later passes launch only the RHS still iterating
+                    a.act = act.get();
+                    nb_launch = *P->h_count;
+                }
             }
         }
         if (P->timing) {

@@ -446,15 +446,41 @@ __global__ void apply_kernel(OpConst op, const double* mu, const double* shift, 
     }
 }
 
-__global__ void count_active_kernel(const RhsState* st, int nb, int* out) {
-    __shared__ int cnt;
-    if (threadIdx.x == 0) cnt = 0;
+__global__ void count_active_kernel(const RhsState* st, int nb, int* out, int32_t* act) {
+    // one block: ordered compaction of the not-done RHS (block-wide exclusive scan per chunk)
+    __shared__ int wsum[32];
+    __shared__ int base;
+    if (threadIdx.x == 0) base = 0;
     __syncthreads();
-    int c = 0;
-    for (int r = threadIdx.x; r < nb; r += blockDim.x) c += st[r].done ? 0 : 1;
-    atomicAdd(&cnt, c);
-    __syncthreads();
-    if (threadIdx.x == 0) *out = cnt;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int c0 = 0; c0 < nb; c0 += blockDim.x) {
+        const int r = c0 + threadIdx.x;
+        const int a = (r < nb && !st[r].done) ? 1 : 0;
+        int x = a;                                            // inclusive warp scan
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int w = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            if (lane < nw) wsum[lane] = w;                    // inclusive warp totals
+        }
+        __syncthreads();
+        const int pos = base + (warp > 0 ? wsum[warp - 1] : 0) + x - a;
+        if (a && act) act[pos] = r;
+        __syncthreads();
+        if (threadIdx.x == 0) base += wsum[nw - 1];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = base;
 }
 
 __global__ void scatter_rhs_kernel(double2* R0, size_t N, long long rg0, int ncols, const int32_t* nodes,
@@ -603,8 +629,8 @@ void launch_cocg_pass(const PassArgs& a, int nb, cudaStream_t s) {
     else launch_pass_impl<false>(a, nb, s);
 }
 
-void launch_count_active(const RhsState* st, int nb, int* d_count, cudaStream_t s) {
-    count_active_kernel<<<1, 256, 0, s>>>(st, nb, d_count);
+void launch_count_active(const RhsState* st, int nb, int* d_count, cudaStream_t s, int32_t* act) {
+    count_active_kernel<<<1, 256, 0, s>>>(st, nb, d_count, act);
     DOT_CUDA_TRY(cudaGetLastError());
 }
 

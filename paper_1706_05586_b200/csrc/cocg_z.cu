@@ -96,7 +96,11 @@ __device__ void zpass_scalars(const PassArgs& a, int rhs, int tile, ZScalars* ou
             cur.alpha_im = alpha.y;
         }
     }
-    if (tile == 0) a.st[a.k & 1][rhs] = cur;
+    if (tile == 0) {
+        a.st[a.k & 1][rhs] = cur;
+        // a finished RHS may drop out of later launches (active list): freeze both copies
+        if (cur.done) a.st[(a.k + 1) & 1][rhs] = cur;
+    }
     *out = sc;
 }
 
@@ -152,7 +156,8 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int PD = NS - 2;                          // TMA planes in flight
     const int ntiles = a.tl.ntiles;
-    const int tile = blockIdx.x % ntiles, zc = a.zc0 + blockIdx.x / ntiles, rhs = blockIdx.y;
+    const int tile = blockIdx.x % ntiles, zc = a.zc0 + blockIdx.x / ntiles;
+    const int rhs = a.act ? a.act[blockIdx.y] : blockIdx.y;       // active-list compaction (tail passes)
     const int nx = a.op.nx, ny = a.op.ny, nz = a.op.nz;
     const int TY = a.tl.TY;
     // z chunk [z0, z1) of this CTA; phase 1 runs on [a1, b1), phase 2 on [a2, b2)

@@ -32,6 +32,7 @@ struct PassArgs {
     int zlen = 0;                 // planes per z chunk
     int zc0 = 0;                  // first (global) z chunk of this launch (z-slab domain decomposition)
     int nzch_tot = 1;             // global z chunks: partial slots per RHS = ntiles * nzch_tot
+    const int32_t* act = nullptr; // z pass: grid row y iterates RHS act[y] (active list), null = identity
     int max_iter = 0;
     double tol2 = 0;              // tol^2
     const double* mu = nullptr;   // [N] absorption
@@ -76,7 +77,8 @@ size_t zpass_smem(int nx, int TY, int NS, int nz);
 void launch_cocg_zpass(const PassArgs& a, int nb, cudaStream_t s);
 void launch_cocg_init(const PassArgs& a, int nb, cudaStream_t s);
 void launch_cocg_pass(const PassArgs& a, int nb, cudaStream_t s);
-void launch_count_active(const RhsState* st, int nb, int* d_count, cudaStream_t s);
+// *d_count = number of RHS not done; act (optional, [nb]) receives their indices in order
+void launch_count_active(const RhsState* st, int nb, int* d_count, cudaStream_t s, int32_t* act = nullptr);
 void launch_apply(const OpConst& op, const double* mu, const double* shift, const double2* u,
                   double2* Au, int nb, cudaStream_t s);
 // Chunk of the global RHS list r = f*ncols + c (r = rg0 .. rg0+nb-1):
