@@ -202,6 +202,13 @@ int dot_dd_fields(dot_dd* G, const double* W, int32_t ls, const double* V, int32
 const char* dot_dd_last_error(const dot_dd* G);
 int dot_dd_destroy(dot_dd* G);
 
+/* prefetch_fields(W, V): solve the forward fields of B W (ls columns; W NULL =
+ * identity; ls = 0: none) and the adjoint fields of C V (ld; likewise) that are not
+ * already cached, all frequencies, in ONE batch (L966: "we solve A(p) z_i = B w_i ...
+ * A^T(p) y_j = C v_j"), so that a following dot_misfit / dot_jacobian /
+ * dot_fields_on_support with these W, V runs without solves. */
+int dot_prefetch_fields(dot_problem* P, const double* W, int32_t ls, const double* V, int32_t ld, int where);
+
 /* ---- component calls (same kernels; used by the parity tests) ---- */
 
 /* mu(x, p) of the last set_params: mu_out [N] real. */

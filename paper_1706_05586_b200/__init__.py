@@ -166,6 +166,15 @@ class DOTProblem:
                                          C.byref(m), rp))
         return (m.value, res) if return_resid else m.value
 
+    def prefetch_fields(self, W=None, V=None, ls=None, ld=None):
+        """Solve the uncached forward fields of B W and adjoint fields of C V in one batch
+        (ls / ld = 0 skips a side; W / V None = identity)."""
+        ls = self.n_src if (W is None and ls is None) else (0 if ls == 0 else (ls if W is None else int(W.shape[1])))
+        ld = self.n_det if (V is None and ld is None) else (0 if ld == 0 else (ld if V is None else int(V.shape[1])))
+        a = _Args(_where_of(W, V))
+        self._check(self._lib.dot_prefetch_fields(self._h, a.ptr(W, np.float64) if ls else None, ls,
+                                                  a.ptr(V, np.float64) if ld else None, ld, a.where))
+
     def jacobian(self, W=None, V=None, where=None):
         """(W^T (x) V^T) J as [n_freq][ld][ls][n_p] complex."""
         ls = self.n_src if W is None else int(W.shape[1])

@@ -69,6 +69,7 @@ SIGNATURES = {
     "dot_dd_fields": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int]),
     "dot_dd_last_error": (C.c_char_p, [C.c_void_p]),
     "dot_dd_destroy": (C.c_int, [C.c_void_p]),
+    "dot_prefetch_fields": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int]),
     "dot_absorption": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     "dot_support": (C.c_int, [C.c_void_p, i32p, C.c_void_p, C.c_void_p, C.c_int]),
     "dot_apply": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int]),

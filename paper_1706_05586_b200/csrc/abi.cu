@@ -1214,6 +1214,23 @@ int dot_optimize_directions_subspace(dot_problem* P, int32_t k, int32_t iters, i
     DOT_API_END(P)
 }
 
+int dot_prefetch_fields(dot_problem* P, const double* W, int32_t ls, const double* V, int32_t ld, int where) {
+    DOT_API_BEGIN
+    if (!P) throw Error(DOT_ERR_ARG, "null problem");
+    require_params(P);
+    std::vector<Req> reqs;
+    if (ls > 0) {
+        check_side_matrix(W, P->n_src, ls, "W");
+        reqs.push_back(Req{0, W ? host_copy(P, W, (size_t)P->n_src * ls, where) : std::vector<double>(), W == nullptr, ls});
+    }
+    if (ld > 0) {
+        check_side_matrix(V, P->n_det, ld, "V");
+        reqs.push_back(Req{1, V ? host_copy(P, V, (size_t)P->n_det * ld, where) : std::vector<double>(), V == nullptr, ld});
+    }
+    prefetch_fields(P, reqs);
+    DOT_API_END(P)
+}
+
 int dot_absorption(dot_problem* P, double* mu_out, int where) {
     DOT_API_BEGIN
     if (!P || !mu_out) throw Error(DOT_ERR_ARG, "null argument");

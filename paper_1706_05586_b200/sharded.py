@@ -111,7 +111,11 @@ def sharded_step(backend, plan: ShardPlan, p, W, V, data=None, device=None):
     Vm[dlo:dhi] = Vn[dlo:dhi]
     Wm, Vm = _as_dev(Wm, Es), _as_dev(Vm, Es)
 
-    # misfit over my source block, all detectors (forward solves of the block)
+    # forward solves of my source block and adjoint solves of my detector block, one batch
+    if hasattr(backend, "prefetch_fields"):
+        backend.prefetch_fields(Es if shi > slo else None, Ed if dhi > dlo else None,
+                                ls=None if shi > slo else 0, ld=None if dhi > dlo else 0)
+    # misfit over my source block, all detectors
     m_part = backend.misfit(Es, None) if shi > slo else 0.0
     m = torch.tensor([m_part], dtype=torch.float64, device=dev)
     tdist.all_reduce(m)

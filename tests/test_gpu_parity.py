@@ -342,3 +342,25 @@ def test_tiling_knobs_keep_parity(dot, knobs, monkeypatch):
     samp = g.samples()
     M = np.transpose(X[:, :, np.searchsorted(samp, wl.det_nodes)], (0, 2, 1))
     assert rel(M, measurements(prob, wl.p)) < 1e-8
+
+
+def test_prefetch_fields_one_batch_then_cached(dot):
+    """dot_prefetch_fields solves B W and C V together; misfit / jacobian /
+    fields_on_support then run without solves and match the oracle."""
+    from oracle import misfit as omisfit
+    cfg = small_config(**GRIDS[3])
+    prob, wl = small_problem(cfg)
+    g = gpu_problem(dot, cfg, prob, wl)
+    rng = np.random.default_rng(2)
+    W = np.sign(rng.standard_normal((cfg.n_s, 3)))
+    V = np.sign(rng.standard_normal((cfg.n_d, 2)))
+    g.reset_stats()
+    g.prefetch_fields(W, V)
+    nf = len(cfg.freqs_hz)
+    assert g.stats()["rhs_solved"] == nf * 5
+    m = g.misfit(W, V)
+    J = g.jacobian(W, V)
+    g.fields_on_support(1, V)
+    assert g.stats()["rhs_solved"] == nf * 5
+    assert abs(m - omisfit(prob, wl.p, W, V)) <= 1e-8 * m
+    assert rel(J, jacobian(prob, wl.p, W, V)) < 1e-7
