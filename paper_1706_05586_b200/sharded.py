@@ -78,7 +78,7 @@ def _as_dev(x, like):
     return t.to(like.device) if like is not None else t
 
 
-def sharded_step(backend, plan: ShardPlan, p, W, V, data=None, device=None):
+def sharded_step(backend, plan: ShardPlan, p, W, V, data=None, device=None, comm_device=None):
     """One step: set_params, all-source + all-detector solves, full-data misfit,
     full Jacobian and the sketched Jacobian (W, V).  Returns a dict with
     misfit, J_full (rank 0), J_sketch, d2h_bytes."""
@@ -96,9 +96,22 @@ def sharded_step(backend, plan: ShardPlan, p, W, V, data=None, device=None):
         return {"misfit": m, "J_full": J_full, "J_sketch": J_sk, "d2h_bytes": d2h}
 
     import torch.distributed as tdist
+    # compute device: where the backend's fields live (CUDA for DOTProblem); comm device:
+    # where the process group wants tensors (CUDA for NCCL, CPU for gloo)
     dev = device
     if dev is None:
         dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu")
+    cdev = comm_device if comm_device is not None else dev
+
+    def T(x):                                   # backend output -> torch tensor on the compute device
+        return x.to(dev) if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x), device=dev)
+
+    def all_reduce_(t):
+        tc = t if t.device == cdev else t.to(cdev)
+        tdist.all_reduce(torch.view_as_real(tc) if tc.is_complex() else tc)
+        if tc is not t:
+            t.copy_(tc)
+
     slo, shi = plan.src_block()
     dlo, dhi = plan.det_block()
     Wn = W.detach().cpu().numpy() if isinstance(W, torch.Tensor) else np.asarray(W)
@@ -118,28 +131,28 @@ def sharded_step(backend, plan: ShardPlan, p, W, V, data=None, device=None):
     # misfit over my source block, all detectors
     m_part = backend.misfit(Es, None) if shi > slo else 0.0
     m = torch.tensor([m_part], dtype=torch.float64, device=dev)
-    tdist.all_reduce(m)
-    # sampled fields of my blocks on S (cached from the solves; detectors solved here)
-    U_blk = backend.fields_on_support(0, Es)          # [nf][ns_r][K]
-    L_blk = backend.fields_on_support(1, Ed)          # [nf][nd_r][K]
+    all_reduce_(m)
+    # sampled fields of my blocks on S (cached from the solves)
+    U_blk = T(backend.fields_on_support(0, Es))       # [nf][ns_r][K]
+    L_blk = T(backend.fields_on_support(1, Ed))       # [nf][nd_r][K]
     # sketched fields: partial combinations of my blocks, summed over ranks
-    UW = backend.fields_on_support(0, Wm)
-    LV = backend.fields_on_support(1, Vm)
+    UW = T(backend.fields_on_support(0, Wm))
+    LV = T(backend.fields_on_support(1, Vm))
     for t in (UW, LV):
-        tdist.all_reduce(torch.view_as_real(t))
-    G = backend.support_weights()
-    J_sk = backend.contract(LV, UW, G)
+        all_reduce_(t)
+    G = T(backend.support_weights())
+    J_sk = T(backend.contract(LV, UW, G))
     # full Jacobian: every source field on S to every rank, rows of my detector block
     nf, K = U_blk.shape[0], U_blk.shape[2]
-    pad = torch.zeros((nf, plan.per_src, K), dtype=U_blk.dtype, device=dev)
-    pad[:, : U_blk.shape[1]] = U_blk
+    pad = torch.zeros((nf, plan.per_src, K), dtype=U_blk.dtype, device=cdev)
+    pad[:, : U_blk.shape[1]] = U_blk.to(cdev)
     parts = [torch.empty_like(pad) for _ in range(plan.world)]
     tdist.all_gather([torch.view_as_real(t) for t in parts], torch.view_as_real(pad))
     U_all = torch.cat([parts[r][:, : plan.src_block(r)[1] - plan.src_block(r)[0]] for r in range(plan.world)], 1)
-    J_rows = backend.contract(L_blk, U_all, G) if dhi > dlo else None   # [nf][nd_r][ns][np]
-    rows = torch.zeros((nf, plan.per_det, plan.n_s, G.shape[1]), dtype=torch.complex128, device=dev)
+    J_rows = T(backend.contract(L_blk, U_all.to(dev), G)) if dhi > dlo else None   # [nf][nd_r][ns][np]
+    rows = torch.zeros((nf, plan.per_det, plan.n_s, G.shape[1]), dtype=torch.complex128, device=cdev)
     if J_rows is not None:
-        rows[:, : J_rows.shape[1]] = J_rows
+        rows[:, : J_rows.shape[1]] = J_rows.to(cdev)
     gathered = [torch.empty_like(rows) for _ in range(plan.world)] if plan.rank == 0 else None
     tdist.gather(torch.view_as_real(rows), [torch.view_as_real(t) for t in gathered] if gathered else None, dst=0)
     J_full = None
