@@ -52,7 +52,6 @@ def _worker(rank, world, port, q):
                                                                    else out["J_full"]),
                "solves": g.stats()["rhs_solved"]}
         q.put(res)
-        tdist.barrier()
         tdist.destroy_process_group()
     except Exception as e:  # pragma: no cover
         import traceback
@@ -69,8 +68,10 @@ def test_two_rank_sharded_step_on_one_gpu():
     for p in procs:
         p.start()
     res = sorted([qu.get(timeout=600) for _ in range(2)], key=lambda r: r["rank"])
-    for p in procs:
-        p.join(timeout=120)
+    for p in procs:            # results are in; do not wait long for process teardown
+        p.join(timeout=20)
+        if p.is_alive():
+            p.kill()
     assert all("error" not in r for r in res), [r.get("error") for r in res]
     cfg = _cfg()
     prob, wl = small_problem(cfg)
