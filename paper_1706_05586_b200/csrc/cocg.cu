@@ -531,19 +531,20 @@ static CocgTiling ring_tiling(int nx, int ny, int nz, int prefetch, size_t max_s
 //   B: 1 row per thread, <= 768 threads, one CTA per SM (78 registers, no spills)
 //   C: 1 row, <= 1024 threads (64 registers)     A: 1 row, <= 512 threads, two CTAs per SM
 //   E: 3 rows, <= 384 threads                     F: 4 rows, <= 256 threads
+//   G: 2 rows, <= 256 threads, two CTAs per SM
 // The first option whose tile height reaches 4 rows wins, else the one with the largest TY.
 // DOT_COCG_ZOPT=A..F forces one option (E and F are only tried when forced).
 static bool z_tiling(int nx, int ny, int nz, int prefetch, int want_ty, CocgTiling& out) {
     const int NS = prefetch + 2;
     const size_t sm_cta = 227 * 1024, sm_sm = 228 * 1024 - 2048;
     struct Opt { char name; int rows, maxt, minb; };
-    const Opt opts[6] = {{'D', 2, 512, 1}, {'B', 1, 768, 1}, {'C', 1, 1024, 1}, {'A', 1, 512, 2},
-                         {'E', 3, 384, 1}, {'F', 4, 256, 1}};
+    const Opt opts[7] = {{'D', 2, 512, 1}, {'B', 1, 768, 1}, {'C', 1, 1024, 1}, {'A', 1, 512, 2},
+                         {'E', 3, 384, 1}, {'F', 4, 256, 1}, {'G', 2, 256, 2}};
     const char* eO = std::getenv("DOT_COCG_ZOPT");
     CocgTiling best;
     bool found = false;
     for (const Opt& o : opts) {
-        if (eO ? eO[0] != o.name : (o.name == 'E' || o.name == 'F')) continue;
+        if (eO ? eO[0] != o.name : (o.name == 'E' || o.name == 'F' || o.name == 'G')) continue;
         int ty = 0;
         for (int c = 1; c <= ny; ++c) {
             const int thr = ((c + 4 + o.rows - 1) / o.rows * nx + 31) / 32 * 32;

@@ -524,7 +524,10 @@ void launch_cocg_zpass(const PassArgs& a, int nb, cudaStream_t s) {
     const int maxt = a.tl.threads;
     if (a.tl.zrows >= 2) {
         if (maxt > 512) throw Error(DOT_ERR_ARG, "z pass with 2..4 rows per thread supports <= 512 threads");
-        if (a.tl.zrows == 2) {
+        if (a.tl.zrows == 2 && a.tl.minb >= 2) {
+            if (a.X) launch_z<true, 512, 1, 2>(a, nb, s);
+            else launch_z<false, 256, 2, 2>(a, nb, s);
+        } else if (a.tl.zrows == 2) {
             if (a.X) launch_z<true, 512, 1, 2>(a, nb, s);
             else launch_z<false, 512, 1, 2>(a, nb, s);
         } else if (a.tl.zrows == 3) {
