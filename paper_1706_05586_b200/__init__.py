@@ -60,7 +60,14 @@ class _Args:
             t = torch.empty(shape, dtype=tdt, device="cuda")
             self.keep.append(t)
             return t, C.c_void_p(t.data_ptr())
-        a = np.empty(shape, dtype=dtype)
+        n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        if n >= (1 << 20):
+            # large host results land in pinned memory (asynchronous DMA, no staging copy)
+            import torch
+            tdt = {np.float64: torch.float64, np.complex128: torch.complex128}[dtype]
+            a = torch.empty(shape, dtype=tdt, pin_memory=torch.cuda.is_available()).numpy()
+        else:
+            a = np.empty(shape, dtype=dtype)
         self.keep.append(a)
         return a, C.c_void_p(a.ctypes.data)
 

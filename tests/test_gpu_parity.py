@@ -364,3 +364,32 @@ def test_prefetch_fields_one_batch_then_cached(dot):
     assert g.stats()["rhs_solved"] == nf * 5
     assert abs(m - omisfit(prob, wl.p, W, V)) <= 1e-8 * m
     assert rel(J, jacobian(prob, wl.p, W, V)) < 1e-7
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_geometries_and_tilings(dot, seed, monkeypatch):
+    """Seeded random grids (odd / even / tiny extents, ragged tiles and chunks) under a
+    random z-pass tiling option: dense solves and sampled measurements vs the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    nx, ny, nz = int(rng.integers(3, 40)), int(rng.integers(3, 40)), int(rng.integers(2, 30))
+    opt = ["A", "B", "C", "D", "E", "F", "G"][seed % 7]
+    monkeypatch.setenv("DOT_COCG_ZOPT", opt)
+    if seed % 3 == 0 and nz >= 8:
+        monkeypatch.setenv("DOT_COCG_ZCHUNKS", str(int(rng.integers(2, 5))))
+    L = (float(rng.uniform(1.5, 4.0)), float(rng.uniform(1.5, 4.0)), float(rng.uniform(1.0, 3.0)))
+    src = (min(2, nx), min(2, ny))
+    det = (min(2, nx), min(3, ny))
+    cfg = small_config(n=(nx, ny, nz), L=L, src=src, det=det, eps=0.5, seed=seed)
+    prob, wl = small_problem(cfg, with_data=False)
+    g = gpu_problem(dot, cfg, prob, wl)
+    N = prob.grid.N
+    b = rng.standard_normal((2, N)) + 1j * rng.standard_normal((2, N))
+    mu = absorption(wl.p, prob.grid, cfg)
+    for f in range(len(prob.omegas)):
+        x, _ = g.solve(b, f)
+        ref = spla.splu(prob.operator(mu, f).tocsc()).solve(b.T).T
+        assert rel(x, ref) < 1e-11, (nx, ny, nz, opt, f)
+    X = g.solve_sampled(0)
+    samp = g.samples()
+    M = np.transpose(X[:, :, np.searchsorted(samp, wl.det_nodes)], (0, 2, 1))
+    assert rel(M, measurements(prob, wl.p)) < 1e-8, (nx, ny, nz, opt)
