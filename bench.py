@@ -394,7 +394,11 @@ def main():
         "mean_iters_per_solve": (st["rhs_iterations"] - s0["rhs_iterations"]) / max(st["rhs_solved"] - s0["rhs_solved"], 1),
         "roofline": roof,
         "jacobian": {"achieved_tflops": jf, "peak_tflops": fpk, "frac": jf / fpk, "peak_source": fsrc,
-                     "support_K": st["support_K"], "flops_per_step": (st["contract_flops"] - s0["contract_flops"]) / args.steps},
+                     "support_K": st["support_K"], "flops_per_step": (st["contract_flops"] - s0["contract_flops"]) / args.steps,
+                     "ms_per_step": (st["contract_ms"] - s0["contract_ms"]) / args.steps,
+                     "dense_equivalent_tflops": st["contract_flops_dense"] / max(st["contract_ms"], 1e-9) / 1e9,
+                     "note": ("block-sparse by basis (PAPER.md L972): useful flops = 4 per (pair, point, parameter) "
+                              "with a nonzero dA/dp block; dense_equivalent counts the K x n_p GEMM it replaces")},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(st["kernel_launches"] - s0["kernel_launches"]),

@@ -85,9 +85,11 @@ typedef struct dot_stats {
     double pass_ms;              /* device time in COCG pass kernels (when timing enabled) */
     double pass_bytes;           /* algorithmic HBM bytes of those passes: 64 B x N x (active RHS) per pass */
     double contract_ms;          /* device time in the Jacobian contraction (timing enabled) */
-    double contract_flops;       /* its algorithmic flops: 2 x 2 x pairs x K x n_p        */
+    double contract_flops;       /* its useful flops: 4 x pairs x (points, parameter) pairs with a
+                                    nonzero dA/dp block (block-sparse by basis, L972)            */
     int32_t support_K;           /* |S|: nodes where dA/dp != 0 after the last set_params */
     int32_t n_samples;           /* |P| = |S u detectors u sources|: nodes where solutions are kept */
+    double contract_flops_dense; /* the dense-equivalent flops 4 x pairs x K x n_p of the same calls */
 } dot_stats;
 
 const char* dot_version(void);

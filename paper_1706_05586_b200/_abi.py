@@ -37,6 +37,7 @@ class DotStats(C.Structure):
         ("pass_ms", C.c_double), ("pass_bytes", C.c_double),
         ("contract_ms", C.c_double), ("contract_flops", C.c_double),
         ("support_K", C.c_int32), ("n_samples", C.c_int32),
+        ("contract_flops_dense", C.c_double),
     ]
 
     def as_dict(self):

@@ -56,6 +56,8 @@ struct dot_problem {
     int K = 0, nP = 0;
     DBuf<int32_t> d_S, d_P, d_S_slot, d_det_slot, d_src_slot, d_off;
     DBuf<double> d_G;
+    DBuf<int32_t> d_seg, d_segoff;    // block sparsity of G by basis (GSparse)
+    GSparse gsp;
     DBuf<double2> d_Dt;               // data, [n_freq][n_src][n_det]
     FieldCache cache[2];              // 0: sources, 1: detectors
 
@@ -1010,12 +1012,34 @@ int dot_set_params(dot_problem* P, const double* p, int where) {
     P->d_src_slot = DBuf<int32_t>(P->arena, P->n_src);
     P->d_off = DBuf<int32_t>(P->arena, (size_t)P->nz * P->tl.ntiles + 1);
     P->d_G = DBuf<double>(P->arena, std::max<size_t>((size_t)P->K * P->n_p, 1));
+    P->d_seg.reset();
+    P->d_segoff.reset();
+    P->gsp = GSparse{};
     launch_compact(P->d_flagS.get(), P->d_posS.get(), N, P->d_S.get(), s);
     launch_compact(P->d_flagP.get(), P->d_posP.get(), N, P->d_P.get(), s);
     launch_gather_rank(P->d_posP.get(), P->d_S.get(), P->K, P->d_S_slot.get(), s);
     launch_gather_rank(P->d_posP.get(), P->d_det.get(), P->n_det, P->d_det_slot.get(), s);
     launch_gather_rank(P->d_posP.get(), P->d_src.get(), P->n_src, P->d_src_slot.get(), s);
     launch_pals_grad(P->pc, P->d_params.get(), P->d_S.get(), P->K, P->d_G.get(), s);
+    {   // block sparsity of G by basis for the Jacobian contraction (L972); DOT_CONTRACT=dense skips it
+        const char* eC = std::getenv("DOT_CONTRACT");
+        const size_t nfl = (size_t)P->n_rbf * P->K;
+        if (nfl > 0 && !(eC && std::string(eC) == "dense")) {
+            DBuf<int32_t> F(P->arena, nfl), Fpos(P->arena, nfl), tmp(P->arena, scan_temp_bytes(nfl) / 4 + 1);
+            launch_rbf_flags(P->d_G.get(), P->K, P->n_rbf, F.get(), s);
+            launch_exclusive_scan(F.get(), Fpos.get(), nfl, P->d_tot.get() + 2, tmp.get(), s);
+            int32_t T = 0;
+            DOT_CUDA_TRY(cudaMemcpyAsync(&T, P->d_tot.get() + 2, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+            sync(P);
+            P->d_seg = DBuf<int32_t>(P->arena, std::max(T, 1));
+            P->d_segoff = DBuf<int32_t>(P->arena, P->n_rbf + 1);
+            launch_rbf_segments(F.get(), Fpos.get(), P->K, P->n_rbf, P->d_tot.get() + 2, P->d_seg.get(),
+                                P->d_segoff.get(), s);
+            P->stats.kernel_launches += 5;
+            sync(P);
+            P->gsp = GSparse{P->d_seg.get(), P->d_segoff.get(), P->n_rbf, T};
+        }
+    }
     launch_sample_offsets(P->d_P.get(), P->nP, P->nx, P->ny, P->nz, P->tl.TY, P->tl.ntiles, P->d_off.get(), s);
     P->stats.kernel_launches += 6;
     sync(P);
@@ -1100,7 +1124,8 @@ int dot_jacobian(dot_problem* P, const double* W, int32_t ls, const double* V, i
         e1 = event_at(P, 1);
         DOT_CUDA_TRY(cudaEventRecord(e0, s));
     }
-    launch_contract(nf, K, ld, ls, P->n_p, LS.get(), (size_t)ld * K, US.get(), (size_t)ls * K, P->d_G.get(), J, s);
+    launch_contract(nf, K, ld, ls, P->n_p, LS.get(), (size_t)ld * K, US.get(), (size_t)ls * K, P->d_G.get(), J, s,
+                    &P->gsp);
     P->stats.kernel_launches += 3;
     if (P->timing) {
         DOT_CUDA_TRY(cudaEventRecord(e1, s));
@@ -1109,7 +1134,10 @@ int dot_jacobian(dot_problem* P, const double* W, int32_t ls, const double* V, i
         DOT_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
         P->stats.contract_ms += ms;
     }
-    P->stats.contract_flops += 4.0 * nf * ld * ls * (double)K * P->n_p;
+    // useful flops: 4 per (pair, point, parameter) with a nonzero weight block (5 per basis
+    // over its points when the block-sparse kernel runs; the dense K x n_p otherwise)
+    P->stats.contract_flops += 4.0 * nf * ld * ls * (P->gsp.seg ? 5.0 * (double)P->gsp.total : (double)K * P->n_p);
+    P->stats.contract_flops_dense += 4.0 * nf * ld * ls * (double)K * P->n_p;
     if (where == DOT_HOST) {
         DOT_CUDA_TRY(cudaMemcpyAsync(J_out, J, nJ * sizeof(double2), cudaMemcpyDeviceToHost, s));
     }
@@ -1130,7 +1158,7 @@ int dot_optimize_directions(dot_problem* P, int32_t k, const double* W, int32_t 
     const double2* XU = get_fields(P, 0, {}, true, P->n_src, t0);
     const double2* XL = get_fields(P, 1, {}, true, P->n_det, t1);
     OptContext oc{P->arena, P->stream, P->n_freq, P->n_src, P->n_det, P->n_p, P->K, P->nP,
-                  XU, XL, P->d_S_slot.get(), P->d_G.get(), &P->stats.kernel_launches};
+                  XU, XL, P->d_S_slot.get(), P->d_G.get(), &P->stats.kernel_launches, &P->gsp};
     double obj = optimize_two_phase(oc, k, hW, ls, hV, ld);
     if (objective_out) *objective_out = obj;
     if (where == DOT_HOST) {
@@ -1200,7 +1228,7 @@ int dot_optimize_directions_subspace(dot_problem* P, int32_t k, int32_t iters, i
         sync(P);
     };
     OptContext oc{P->arena, P->stream, P->n_freq, P->n_src, P->n_det, P->n_p, P->K, P->nP,
-                  nullptr, nullptr, P->d_S_slot.get(), P->d_G.get(), &P->stats.kernel_launches};
+                  nullptr, nullptr, P->d_S_slot.get(), P->d_G.get(), &P->stats.kernel_launches, &P->gsp};
     double obj = optimize_two_phase_subspace(oc, ops, k, iters, block, hW, ls, hV, ld, hXs, hXd);
     if (objective_out) *objective_out = obj;
     if (where == DOT_HOST) {

@@ -162,14 +162,170 @@ void launch_nt(int nb, int K, int ld, int ls, int n_p, const double2* Lam, size_
     DOT_CUDA_TRY(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------- block-sparse
+// Per basis j (grid.y) the 5 parameter columns 5j..5j+4 (one n8 fragment, 3 zero
+// columns) over the support points of that basis only.  Same GEMM view and DMMA
+// fragments as above; k-tiles of SBK points taken from the segment list.
+constexpr int SBK = 32;
+constexpr int SAS = SBK + 4;
+constexpr int SGS = 8 + 4;
+constexpr int SHPT = (BM / 2) * SBK / THREADS;   // Hadamard products per thread per k-tile (8)
+
+__global__ void __launch_bounds__(THREADS) contract_sparse_kernel(int K, int ld, int ls, int n_p,
+                                                                  const double2* __restrict__ Lam, size_t lam_bs,
+                                                                  const double2* __restrict__ U, size_t u_bs,
+                                                                  const double* __restrict__ G,
+                                                                  const int32_t* __restrict__ seg,
+                                                                  const int32_t* __restrict__ segoff, double2* J) {
+    extern __shared__ __align__(16) double csm[];
+    auto Abuf = [&](int bb) { return csm + bb * (BM * SAS); };
+    auto Gbuf = [&](int bb) { return csm + 2 * BM * SAS + bb * (SBK * SGS); };
+    const int b = blockIdx.z, jb = blockIdx.y;
+    const int npairs = ld * ls;
+    const int pair0 = blockIdx.x * (BM / 2);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double2* Lb = Lam + (size_t)b * lam_bs;
+    const double2* Ub = U + (size_t)b * u_bs;
+    const int s0 = segoff[jb], s1 = segoff[jb + 1];
+    const int c0 = 5 * jb;
+
+    const double2* lrow[SHPT];
+    const double2* urow[SHPT];
+    bool pv[SHPT];
+#pragma unroll
+    for (int q = 0; q < SHPT; ++q) {
+        const int e = threadIdx.x + q * THREADS;
+        const int pair = pair0 + e / SBK;
+        pv[q] = pair < npairs;
+        const int j = pv[q] ? pair / ls : 0, i = pv[q] ? pair - j * ls : 0;
+        lrow[q] = Lb + (size_t)j * K;
+        urow[q] = Ub + (size_t)i * K;
+    }
+    double2 lv[SHPT], uv[SHPT];
+    double gv = 0.0;
+    auto load = [&](int kt) {
+#pragma unroll
+        for (int q = 0; q < SHPT; ++q) {
+            const int t = kt + ((threadIdx.x + q * THREADS) % SBK);
+            const bool ok = pv[q] && t < s1;
+            const int node = ok ? seg[t] : 0;
+            lv[q] = ok ? lrow[q][node] : make_double2(0.0, 0.0);
+            uv[q] = ok ? urow[q][node] : make_double2(0.0, 0.0);
+        }
+        {   // G tile: SBK points x 8 columns (5 used) = 256 values, one per thread
+            const int kk = threadIdx.x / 8, n = threadIdx.x % 8;
+            const int t = kt + kk;
+            gv = (t < s1 && n < 5 && c0 + n < n_p) ? G[(size_t)seg[t] * n_p + c0 + n] : 0.0;
+        }
+    };
+    auto store = [&](int buf) {
+        double* A = Abuf(buf);
+#pragma unroll
+        for (int q = 0; q < SHPT; ++q) {
+            const int e = threadIdx.x + q * THREADS;
+            const int lp = e / SBK, kk = e % SBK;
+            const double2 v = cmul(lv[q], uv[q]);
+            A[(2 * lp) * SAS + kk] = v.x;
+            A[(2 * lp + 1) * SAS + kk] = v.y;
+        }
+        Gbuf(buf)[(threadIdx.x / 8) * SGS + (threadIdx.x % 8)] = gv;
+    };
+
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    if (s0 < s1) {
+        load(s0);
+        store(0);
+    }
+    __syncthreads();
+    int buf = 0;
+    for (int kt = s0; kt < s1; kt += SBK) {
+        const bool more = kt + SBK < s1;
+        if (more) load(kt + SBK);
+        const double* A = Abuf(buf);
+        const double* Bt = Gbuf(buf);
+#pragma unroll
+        for (int k4 = 0; k4 < SBK; k4 += 4) {
+            const double bf = Bt[(k4 + (lane & 3)) * SGS + (lane >> 2)];
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi)
+                dmma(acc[mi][0], acc[mi][1], A[(warp * 16 + mi * 8 + (lane >> 2)) * SAS + k4 + (lane & 3)], bf);
+        }
+        if (more) store(buf ^ 1);
+        __syncthreads();
+        buf ^= 1;
+    }
+    double* Jd = reinterpret_cast<double*>(J);
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+        const int m = warp * 16 + mi * 8 + (lane >> 2);
+        const int pair = pair0 + (m >> 1), c = m & 1;
+        if (pair >= npairs) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int n = 2 * (lane & 3) + h;
+            if (n < 5 && c0 + n < n_p) Jd[(((size_t)b * npairs + pair) * n_p + c0 + n) * 2 + c] = -acc[mi][h];
+        }
+    }
+}
+
+__global__ void rbf_flags_kernel(const double* __restrict__ G, int K, int n_p, int n_rbf, int32_t* F) {
+    const size_t tot = (size_t)K * n_rbf;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
+        const int j = (int)(e / K), s = (int)(e % K);
+        bool nz = false;
+        for (int q = 0; q < 5 && 5 * j + q < n_p; ++q) nz |= G[(size_t)s * n_p + 5 * j + q] != 0.0;
+        F[e] = nz ? 1 : 0;
+    }
+}
+
+__global__ void rbf_segments_kernel(const int32_t* F, const int32_t* pos, int K, int n_rbf, const int32_t* total,
+                                    int32_t* seg, int32_t* off) {
+    const size_t tot = (size_t)K * n_rbf;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
+        if (F[e]) seg[pos[e]] = (int32_t)(e % K);
+        if (e % K == 0) off[e / K] = pos[e];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) off[n_rbf] = *total;
+}
+
 }  // namespace
 
+void launch_rbf_flags(const double* G, int K, int n_rbf, int32_t* F, cudaStream_t s) {
+    const size_t tot = (size_t)K * n_rbf;
+    if (!tot) return;
+    rbf_flags_kernel<<<(unsigned)std::min<size_t>((tot + 255) / 256, 8192), 256, 0, s>>>(G, K, 5 * n_rbf, n_rbf, F);
+    DOT_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_rbf_segments(const int32_t* F, const int32_t* pos, int K, int n_rbf, const int32_t* total, int32_t* seg,
+                         int32_t* off, cudaStream_t s) {
+    const size_t tot = (size_t)K * n_rbf;
+    rbf_segments_kernel<<<(unsigned)std::max<size_t>(1, std::min<size_t>((tot + 255) / 256, 8192)), 256, 0, s>>>(
+        F, pos, K, n_rbf, total, seg, off);
+    DOT_CUDA_TRY(cudaGetLastError());
+}
+
 void launch_contract(int nb, int K, int ld, int ls, int n_p, const double2* Lam, size_t lam_bstride,
-                     const double2* U, size_t u_bstride, const double* G, double2* J, cudaStream_t s) {
+                     const double2* U, size_t u_bstride, const double* G, double2* J, cudaStream_t s,
+                     const GSparse* sp) {
     const int npairs = ld * ls;
     if (nb <= 0 || npairs <= 0 || n_p <= 0) return;
     if (K <= 0) {
         DOT_CUDA_TRY(cudaMemsetAsync(J, 0, (size_t)nb * npairs * n_p * sizeof(double2), s));
+        return;
+    }
+    if (sp && sp->seg && sp->n_rbf * 5 == n_p) {
+        dim3 grid((npairs + BM / 2 - 1) / (BM / 2), sp->n_rbf, nb);
+        const size_t smem = (size_t)(2 * BM * SAS + 2 * SBK * SGS) * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            DOT_CUDA_TRY(cudaFuncSetAttribute(contract_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)smem));
+            attr = true;
+        }
+        contract_sparse_kernel<<<grid, THREADS, smem, s>>>(K, ld, ls, n_p, Lam, lam_bstride, U, u_bstride, G, sp->seg,
+                                                           sp->segoff, J);
+        DOT_CUDA_TRY(cudaGetLastError());
         return;
     }
     // all parameters of a column block in one CTA (one Hadamard formation per pair)

@@ -112,9 +112,25 @@ void launch_sample_offsets(const int32_t* P, int nP, int nx, int ny, int nz, int
                            int32_t* off, cudaStream_t s);
 
 // ------------------------------------------------------------------ contract.cu
+// Block sparsity of G by RBF ("we first find the few nonzero components
+// of dA/dp_k"): seg[segoff[j] .. segoff[j+1]) lists the support points (indices into S,
+// ascending) where the 5 parameters of basis j have nonzero weights.
+struct GSparse {
+    const int32_t* seg = nullptr;
+    const int32_t* segoff = nullptr;   // [n_rbf + 1]
+    int n_rbf = 0;
+    long long total = 0;               // segoff[n_rbf]
+};
+// sp == null (or no segments): dense DMMA contraction over all K points; else the
+// block-sparse one (per basis j, its support points only).
 void launch_contract(int nb, int K, int ld, int ls, int n_p, const double2* Lam, size_t lam_bstride,
                      const double2* U, size_t u_bstride, const double* G, double2* J,
-                     cudaStream_t s);
+                     cudaStream_t s, const GSparse* sp = nullptr);
+// flags F[j][s] = any(G[s][5j .. 5j+4] != 0), j < n_rbf
+void launch_rbf_flags(const double* G, int K, int n_rbf, int32_t* F, cudaStream_t s);
+// out[pos[i]] = i % K for flagged i (segment lists), off[j] = pos[j*K], off[n_rbf] = *total
+void launch_rbf_segments(const int32_t* F, const int32_t* pos, int K, int n_rbf, const int32_t* total,
+                         int32_t* seg, int32_t* off, cudaStream_t s);
 
 // ------------------------------------------------------------------ smallops.cu
 // out[b][m][n] = sum_k Rm[k*ldr + m] * Cx[b*sb + k*sk + n*sn]   (real^T x complex)

@@ -17,6 +17,7 @@ struct OptContext {
     const int32_t* S_slot;    // [K] sample slot of each support node
     const double* G;          // [K][n_p]
     int64_t* launches;
+    const GSparse* gsp = nullptr;   // block sparsity of G (null: dense contraction)
 };
 
 // Two-phase alternating replacement of k directions; W (ns x ls) and V (nd x ld)

@@ -393,3 +393,26 @@ def test_random_geometries_and_tilings(dot, seed, monkeypatch):
     samp = g.samples()
     M = np.transpose(X[:, :, np.searchsorted(samp, wl.det_nodes)], (0, 2, 1))
     assert rel(M, measurements(prob, wl.p)) < 1e-8, (nx, ny, nz, opt)
+
+
+def test_block_sparse_contraction_equals_dense(dot, monkeypatch):
+    """The block-sparse Jacobian contraction (per basis over its own support points,
+    PAPER.md L972) equals the dense K x n_p contraction and the oracle."""
+    cfg = small_config(n=(20, 18, 12), L=(4.0, 3.5, 3.0), src=(3, 2), det=(2, 3), n_rbf=5, eps=0.5)
+    prob, wl = small_problem(cfg)
+    rng = np.random.default_rng(6)
+    W = np.sign(rng.standard_normal((cfg.n_s, 3)))
+    V = np.sign(rng.standard_normal((cfg.n_d, 4)))
+    g = gpu_problem(dot, cfg, prob, wl)
+    g.reset_stats()
+    Js = g.jacobian(W, V)
+    st = g.stats()
+    assert st["contract_flops"] < st["contract_flops_dense"]     # the sparse kernel ran
+    monkeypatch.setenv("DOT_CONTRACT", "dense")
+    gd = gpu_problem(dot, cfg, prob, wl)
+    gd.reset_stats()
+    Jd = gd.jacobian(W, V)
+    std = gd.stats()
+    assert std["contract_flops"] == std["contract_flops_dense"]
+    assert rel(Js, Jd) < 1e-12
+    assert rel(Js, jacobian(prob, wl.p, W, V)) < 1e-7
