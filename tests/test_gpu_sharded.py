@@ -27,7 +27,8 @@ def _cfg():
     return small_config(n=(16, 14, 12), L=(4.0, 3.5, 3.0), src=(3, 2), det=(2, 3), eps=0.4)
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, data):
+    # (the oracle data are computed in the parent: scipy in spawned CUDA workers is slow)
     try:
         import torch.distributed as tdist
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -35,14 +36,16 @@ def _worker(rank, world, port, q):
         tdist.init_process_group("gloo", rank=rank, world_size=world)
         import paper_1706_05586_b200 as dot
         from paper_1706_05586_b200.sharded import ShardPlan, sharded_step
+        from synth import make_workload
         cfg = _cfg()
-        prob, wl = small_problem(cfg)
+        wl = make_workload(cfg)
+        wl.p[0] = max(wl.p[0], 0.8)        # as tests._small.small_problem
         rng = np.random.default_rng(0)
         W = np.sign(rng.standard_normal((cfg.n_s, 3)))
         V = np.sign(rng.standard_normal((cfg.n_d, 2)))
         g = dot.DOTProblem.from_config(cfg, wl.src_nodes, wl.det_nodes)
         plan = ShardPlan(rank, world, cfg.n_s, cfg.n_d)
-        out = sharded_step(g, plan, wl.p, W, V, data=prob.data, device=torch.device("cuda", 0),
+        out = sharded_step(g, plan, wl.p, W, V, data=data, device=torch.device("cuda", 0),
                            comm_device=torch.device("cpu"))
         Js = out["J_sketch"]
         res = {"rank": rank, "misfit": out["misfit"],
@@ -64,7 +67,8 @@ def test_two_rank_sharded_step_on_one_gpu():
     ctx = mp.get_context("spawn")
     qu = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, qu)) for r in range(2)]
+    prob0, _ = small_problem(_cfg())
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, qu, prob0.data)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted([qu.get(timeout=600) for _ in range(2)], key=lambda r: r["rank"])
