@@ -884,10 +884,7 @@ int dot_create(const dot_config* cfg, dot_problem** out) {
 
 int dot_destroy(dot_problem* P) {
     if (!P) return DOT_OK;
-    try {
-        if (P->stream || true) cudaStreamSynchronize(P->stream);
-    } catch (...) {
-    }
+    cudaStreamSynchronize(P->stream);   // outstanding work may still use the bound workspace
     delete P;
     return DOT_OK;
 }
