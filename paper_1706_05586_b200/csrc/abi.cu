@@ -65,11 +65,14 @@ struct dot_problem {
     dot_stats stats{};
     bool timing = false;
     std::vector<cudaEvent_t> events;
-    int* h_count = nullptr;
+    int* h_count = nullptr;          // [2] pinned, pipelined convergence polls
+    cudaEvent_t poll_ev[2] = {nullptr, nullptr};
     int num_sms = 148;
 
     ~dot_problem() {
         for (auto e : events) cudaEventDestroy(e);
+        for (auto e : poll_ev)
+            if (e) cudaEventDestroy(e);
         if (h_count) cudaFreeHost(h_count);
     }
 };
@@ -281,30 +284,39 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, i
 
         launch_cocg_init(a, nb, P->stream);
         P->stats.kernel_launches++;
-        int k = 0;
+        // Groups of CHK passes; each ends with a convergence count into pinned memory.  The
+        // poll is pipelined: group g+1 is enqueued before the host reads group g-1's count,
+        // so the GPU never idles on the host round trip (a group launched after the last
+        // RHS finished runs as no-ops).
+        int k = 0, g = 0;
         size_t ev = 0;
         for (;;) {
-            if (P->timing && k % CHK == 0) DOT_CUDA_TRY(cudaEventRecord(event_at(P, ev++), P->stream));
-            a.k = k;
-            launch_cocg_pass(a, nb_launch, P->stream);
-            P->stats.kernel_launches++;
-            P->stats.pass_launches++;
-            ++k;
-            if (k % CHK == 0 || k > P->max_iter) {
-                if (P->timing) DOT_CUDA_TRY(cudaEventRecord(event_at(P, ev++), P->stream));
-                launch_count_active(a.st[(k - 1) & 1], nb, P->d_count.get(), P->stream,
-                                    P->tl.kind == 1 ? act.get() : nullptr);
+            if (P->timing) DOT_CUDA_TRY(cudaEventRecord(event_at(P, ev++), P->stream));
+            for (int i = 0; i < CHK; ++i) {
+                a.k = k++;
+                launch_cocg_pass(a, nb_launch, P->stream);
                 P->stats.kernel_launches++;
-                DOT_CUDA_TRY(cudaMemcpyAsync(P->h_count, P->d_count.get(), sizeof(int), cudaMemcpyDeviceToHost,
-                                             P->stream));
-                sync(P);
-                if (*P->h_count == 0) break;
+                P->stats.pass_launches++;
+            }
+            if (P->timing) DOT_CUDA_TRY(cudaEventRecord(event_at(P, ev++), P->stream));
+            launch_count_active(a.st[(k - 1) & 1], nb, P->d_count.get() + (g & 1), P->stream,
+                                P->tl.kind == 1 ? act.get() : nullptr);
+            P->stats.kernel_launches++;
+            DOT_CUDA_TRY(cudaMemcpyAsync(P->h_count + (g & 1), P->d_count.get() + (g & 1), sizeof(int),
+                                         cudaMemcpyDeviceToHost, P->stream));
+            DOT_CUDA_TRY(cudaEventRecord(P->poll_ev[g & 1], P->stream));
+            if (g > 0) {
+                DOT_CUDA_TRY(cudaEventSynchronize(P->poll_ev[(g - 1) & 1]));
+                const int c = P->h_count[(g - 1) & 1];
+                if (c == 0) break;
                 if (P->tl.kind == 1) {     // later passes launch only the RHS still iterating
                     a.act = act.get();
-                    nb_launch = *P->h_count;
+                    nb_launch = c;
                 }
             }
+            ++g;
         }
+        sync(P);
         if (P->timing) {
             for (size_t e = 0; e + 1 < ev; e += 2) {
                 float ms = 0;
@@ -868,7 +880,8 @@ int dot_create(const dot_config* cfg, dot_problem** out) {
         }
         P->pc = PalsConst{P->nx, P->ny, P->nz, P->n_rbf, P->hx, P->hy, P->hz, P->gamma, P->eps, P->cutoff,
                           P->mua_in, P->mua_out};
-        DOT_CUDA_TRY(cudaMallocHost(&P->h_count, sizeof(int)));
+        DOT_CUDA_TRY(cudaMallocHost(&P->h_count, 2 * sizeof(int)));
+        for (auto& e : P->poll_ev) DOT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         {
             int dev = 0;
             DOT_CUDA_TRY(cudaGetDevice(&dev));

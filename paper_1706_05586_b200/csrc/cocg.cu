@@ -480,6 +480,8 @@ __global__ void count_active_kernel(const RhsState* st, int nb, int* out, int32_
         if (threadIdx.x == 0) base += wsum[nw - 1];
         __syncthreads();
     }
+    if (act)   // entries past the count: no RHS (a pass launched with an older, larger count skips them)
+        for (int y = base + threadIdx.x; y < nb; y += blockDim.x) act[y] = -1;
     if (threadIdx.x == 0) *out = base;
 }
 

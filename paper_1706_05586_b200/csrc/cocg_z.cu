@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a
     const int ntiles = a.tl.ntiles;
     const int tile = blockIdx.x % ntiles, zc = a.zc0 + blockIdx.x / ntiles;
     const int rhs = a.act ? a.act[blockIdx.y] : blockIdx.y;       // active-list compaction (tail passes)
+    if (rhs < 0) return;                                           // slot past the active count
     const int nx = a.op.nx, ny = a.op.ny, nz = a.op.nz;
     const int TY = a.tl.TY;
     // z chunk [z0, z1) of this CTA; phase 1 runs on [a1, b1), phase 2 on [a2, b2)
