@@ -416,3 +416,21 @@ def test_block_sparse_contraction_equals_dense(dot, monkeypatch):
     assert std["contract_flops"] == std["contract_flops_dense"]
     assert rel(Js, Jd) < 1e-12
     assert rel(Js, jacobian(prob, wl.p, W, V)) < 1e-7
+
+
+def test_block_sparse_gemm_contraction_equals_dense(dot, monkeypatch):
+    """Large panels (ld >= 32, ls >= 8) take the per-(frequency, basis) complex GEMM
+    form of the block-sparse contraction: equal to the dense kernel and the oracle."""
+    cfg = small_config(n=(24, 20, 10), L=(4.0, 3.5, 2.5), src=(3, 3), det=(8, 5), n_rbf=5, eps=0.5)
+    prob, wl = small_problem(cfg)
+    g = gpu_problem(dot, cfg, prob, wl)
+    g.reset_stats()
+    Js = g.jacobian(None, None)                     # ld = 40, ls = 9
+    st = g.stats()
+    assert st["contract_flops"] < st["contract_flops_dense"]
+    monkeypatch.setenv("DOT_CONTRACT", "dense")
+    gd = gpu_problem(dot, cfg, prob, wl)
+    Jd = gd.jacobian(None, None)
+    assert rel(Js, Jd) < 1e-12
+    Jo = jacobian(prob, wl.p, np.eye(cfg.n_s), np.eye(cfg.n_d))
+    assert rel(Js, Jo) < 1e-7
