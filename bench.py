@@ -201,9 +201,17 @@ def main():
     import paper_1706_05586_b200 as dot
     from synth import config_by_name, make_workload
 
+    # DOT_BENCH_BACKEND=gloo + DOT_BENCH_DEVICE=0: smoke-test the multi-rank path with all
+    # ranks on one GPU (collectives through host memory; timings then mean nothing)
+    backend_name = os.environ.get("DOT_BENCH_BACKEND", "nccl")
+    if os.environ.get("DOT_BENCH_DEVICE") is not None:
+        local = int(os.environ["DOT_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     if world > 1:
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend_name == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            tdist.init_process_group(backend_name)
     cfg = config_by_name(args.config)
     wl = make_workload(cfg)
     dev = torch.device("cuda", local)
@@ -238,7 +246,8 @@ def main():
 
     if cfg.name == "full64":
         def run_step(p, W, V, data=None):
-            return sharded_step(gp, plan, p, W, V, data=data)
+            return sharded_step(gp, plan, p, W, V, data=data,
+                                comm_device=None if backend_name == "nccl" else torch.device("cpu"))
     elif cfg.name == "all128":
         if world > 1:
             raise SystemExit("bench: all128 runs single-GPU here")
@@ -371,12 +380,12 @@ def main():
         Usup = gp.fields_on_support(0, None, where=1)
         Gsup = gp.support_weights()
         for _ in range(2):
-            gp.contract(Lsup, Usup, Gsup)
+            dot.contract(Lsup, Usup, Gsup, stream=stream)          # stateless dense DMMA kernel
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         reps = 5
         for _ in range(reps):
-            gp.contract(Lsup, Usup, Gsup)
+            dot.contract(Lsup, Usup, Gsup, stream=stream)
         e1.record(stream)
         torch.cuda.synchronize()
         gms = e0.elapsed_time(e1) / reps

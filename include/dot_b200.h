@@ -241,6 +241,14 @@ int dot_fields_on_support(dot_problem* P, int32_t side, const double* coeff, int
 /* Sample nodes P = S u detectors u sources (ascending, [n_samples] int64). */
 int dot_samples(dot_problem* P, int32_t* n_out, int64_t* nodes_out, int where);
 
+/* Jacobian contraction of explicit field panels on P's support S with P's weights
+ * (block-sparse by basis when available, as dot_jacobian):
+ *   J[f][j][i][k] = - sum_s Lam[f][j][s] U[f][i][s] G[s][k]
+ * Lam [n_freq][ld][K], U [n_freq][ls][K], J [n_freq][ld][ls][n_p] complex, DEVICE
+ * pointers (K = |S| of the last set_params).  Used by the multi-GPU step on
+ * all-reduced / all-gathered fields.  Counts in dot_stats like dot_jacobian. */
+int dot_contract_fields(dot_problem* P, int32_t ld, int32_t ls, const double* Lam, const double* U, double* J);
+
 /* Stateless Jacobian contraction on explicit panels (no problem needed):
  *   J[b][j][i][k] = - sum_s Lam[b][j][s] U[b][i][s] G[s][k]
  * Lam [nb][ld][K], U [nb][ls][K] complex, G [K][n_p] real, J [nb][ld][ls][n_p]

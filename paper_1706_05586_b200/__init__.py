@@ -260,9 +260,21 @@ class DOTProblem:
                                                     xp))
         return X
 
-    def contract(self, Lam, U, G):
-        """DMMA contraction on this problem's stream (see module-level contract)."""
-        return contract(Lam, U, G, stream=self.stream)
+    def contract(self, Lam, U, G=None):
+        """J[f][j][i][k] = -sum_s Lam[f][j][s] U[f][i][s] G[s][k] with this problem's support
+        weights G (block-sparse by basis), on its stream: Lam [n_freq][ld][K], U [n_freq][ls][K]
+        CUDA complex128 tensors.  (G is accepted for interface symmetry and must be the
+        problem's own support weights.)"""
+        import torch
+        Lam, U = Lam.contiguous(), U.contiguous()
+        nf, ld, K = Lam.shape
+        ls = U.shape[1]
+        if nf != self.n_freq or U.shape[0] != nf or U.shape[2] != K:
+            raise ValueError("panels must be [n_freq][cols][K] on this problem's support")
+        J = torch.empty((nf, ld, ls, self.n_p), dtype=torch.complex128, device=Lam.device)
+        self._check(self._lib.dot_contract_fields(self._h, int(ld), int(ls), C.c_void_p(Lam.data_ptr()),
+                                                  C.c_void_p(U.data_ptr()), C.c_void_p(J.data_ptr())))
+        return J
 
     def samples(self):
         n = C.c_int32()

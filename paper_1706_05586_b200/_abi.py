@@ -78,6 +78,7 @@ SIGNATURES = {
     "dot_solve_sampled": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int, C.c_void_p]),
     "dot_samples": (C.c_int, [C.c_void_p, i32p, C.c_void_p, C.c_int]),
     "dot_fields_on_support": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int, C.c_void_p]),
+    "dot_contract_fields": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "dot_contract": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "dot_sym_eig": (C.c_int, [C.c_int, dp, dp, dp]),

@@ -1479,6 +1479,34 @@ int dot_dd_fields(dot_dd* G, const double* W, int32_t ls, const double* V, int32
     }
 }
 
+int dot_contract_fields(dot_problem* P, int32_t ld, int32_t ls, const double* Lam, const double* U, double* J) {
+    DOT_API_BEGIN
+    if (!P || !Lam || !U || !J || ld < 1 || ls < 1) throw Error(DOT_ERR_ARG, "bad argument");
+    require_params(P);
+    const int nf = P->n_freq, K = P->K;
+    cudaStream_t s = P->stream;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (P->timing) {
+        e0 = event_at(P, 0);
+        e1 = event_at(P, 1);
+        DOT_CUDA_TRY(cudaEventRecord(e0, s));
+    }
+    launch_contract(nf, K, ld, ls, P->n_p, reinterpret_cast<const double2*>(Lam), (size_t)ld * K,
+                    reinterpret_cast<const double2*>(U), (size_t)ls * K, P->d_G.get(), reinterpret_cast<double2*>(J), s,
+                    &P->gsp);
+    P->stats.kernel_launches++;
+    if (P->timing) {
+        DOT_CUDA_TRY(cudaEventRecord(e1, s));
+        DOT_CUDA_TRY(cudaEventSynchronize(e1));
+        float ms = 0;
+        DOT_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+        P->stats.contract_ms += ms;
+    }
+    P->stats.contract_flops += 4.0 * nf * ld * ls * (P->gsp.seg ? 5.0 * (double)P->gsp.total : (double)K * P->n_p);
+    P->stats.contract_flops_dense += 4.0 * nf * ld * ls * (double)K * P->n_p;
+    DOT_API_END(P)
+}
+
 int dot_contract(void* stream, int32_t nb, int32_t K, int32_t ld, int32_t ls, int32_t n_p, const double* Lam,
                  const double* U, const double* G, double* J) {
     try {
