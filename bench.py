@@ -59,12 +59,19 @@ class ClockSampler:
         self.proc = None
 
     def start(self):
+        if os.environ.get("DOT_BENCH_NO_CLOCKS") == "1":      # diagnostics only: no sampling
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                  "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi's own start-up (NVML init) stalls the driver for ~100 ms: wait for its
+            # first sample so that it lands before the timed region, not inside it
+            t0 = time.perf_counter()
+            while not self.rows and self.proc.poll() is None and time.perf_counter() - t0 < 10:
+                time.sleep(0.01)
         except FileNotFoundError:
             self.proc = None
 
