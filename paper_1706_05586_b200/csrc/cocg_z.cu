@@ -152,7 +152,7 @@ __device__ __forceinline__ double2 stencil_int(const OpConst& op, double shift, 
 // RPT: slot rows per thread (a thread owns rows RPT*m .. RPT*m + RPT - 1 of one column; the
 // y-neighbours inside its strip come from registers).
 template <bool FULLX, int MAXT, int MINB, int NS, bool MUT, int RPT, bool ZC>
-__global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const PassArgs a) {
+__global__ void __launch_bounds__(MAXT, MINB) cocg_zpass_kernel(const __grid_constant__ PassArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int PD = NS - 2;                          // TMA planes in flight
     const int ntiles = a.tl.ntiles;
