@@ -361,6 +361,8 @@ def main():
         e2e_ev0.record(stream)
         d2h = 0
         for _ in range(args.steps):
+            if flush is not None:
+                flush.zero_()                                     # same L2 hygiene as the device-timed loop
             r = run_step(p_h, W_h, V_h, data=D_h)
             d2h = r["d2h_bytes"]
         e2e_ev1.record(stream)
