@@ -141,3 +141,60 @@ def test_all128_point_solves_true_residual_and_sampled():
         for r in range(len(cols)):
             assert np.linalg.norm(b[r] - A @ x[r]) / np.linalg.norm(b[r]) < 1e-14
             assert np.abs(Xs[f, r] - x[r][samp]).max() <= 1e-10 * np.abs(x[r][samp]).max()
+
+
+def test_opt96_step_optimized_directions_full_size():
+    """configs[3] (`opt96`: 96^3, 1024 x 1024, 5 frequencies, 120 parameters) in the bench
+    step's launch configuration: J(W,V) and misfit, then 2 optimized directions by 5
+    subspace iterations with block 2 (reading R16).  Checked at full size:
+      * the returned objective is ||(W^T (x) V^T) J||_F^2 of the returned W, V (PAPER.md
+        Eq. (maxprob), L466-468) as the Jacobian call computes it;
+      * the kept columns stay in the span of the random ones (remove steps, Th. 3.4/3.5)
+        and the added ones have length sqrt(n) (reading R15);
+      * J(W_hat, V_hat) entries against the direct sum over dense fields of the new
+        directions (L966-972) with the oracle's dA/dp weights, the dense fields pinned
+        by their true residual under the oracle operator (Eq. (2.1))."""
+    from paper_1706_05586_b200 import build
+    build.build()
+    import paper_1706_05586_b200 as dot
+    from oracle import assemble, frob_objective
+    cfg = config_by_name("opt96")
+    wl = make_workload(cfg)
+    g = dot.DOTProblem.from_config(cfg, wl.src_nodes, wl.det_nodes)
+    g.set_params(wl.p)
+    g.set_data(np.zeros((cfg.n_freq, cfg.n_d, cfg.n_s), complex))   # data values do not enter J
+    g.jacobian(wl.W, wl.V)
+    g.misfit(wl.W, wl.V)
+    W2, V2, obj = g.optimize_directions_subspace(cfg.n_opt, wl.W, wl.V, wl.X0_src, wl.X0_det,
+                                                 iters=cfg.n_subspace_iters)
+    J2 = g.jacobian(W2, V2)                          # [f][ld][ls][n_p]
+    assert abs(obj - frob_objective(J2)) <= 1e-9 * obj
+    k = cfg.n_opt
+    for A, M, n in ((W2, wl.W, cfg.n_s), (V2, wl.V, cfg.n_d)):
+        Q, _ = np.linalg.qr(M)
+        kept = A[:, :-k]
+        assert np.linalg.norm(kept - Q @ (Q.T @ kept)) <= 1e-10 * np.linalg.norm(kept)
+        assert np.allclose(np.linalg.norm(A[:, -k:], axis=0), np.sqrt(n), rtol=1e-12)
+    grid = make_grid(cfg.n, cfg.L)
+    N = grid.N
+    mu = absorption(wl.p, grid, cfg)
+    Gfull = jacobian_weights(wl.p, grid, cfg)
+    S = np.nonzero(np.abs(Gfull).sum(1) > 0)[0]
+    scale = grid.theta[wl.src_nodes] / grid.cell_volume
+    f = 2
+    A = assemble(grid, cfg.D, mu, 2 * np.pi * cfg.freqs_hz[f], cfg.nu).tocsr()
+    icol, jcol = [W2.shape[1] - 1, 0], [V2.shape[1] - 2, 3]     # optimized and random columns
+    b = np.zeros((2, N), complex)
+    c = np.zeros((2, N), complex)
+    for r, i in enumerate(icol):
+        np.add.at(b[r], wl.src_nodes, W2[:, i] * scale)
+    for r, j in enumerate(jcol):
+        np.add.at(c[r], wl.det_nodes, V2[:, j])
+    z, _ = g.solve(b, f)
+    y, _ = g.solve(c, f)
+    for rhs, sol in ((b, z), (c, y)):
+        for r in range(2):
+            assert np.linalg.norm(rhs[r] - A @ sol[r]) <= 1e-14 * np.linalg.norm(rhs[r])
+    ref = -np.einsum("jx,xk,ix->jik", y[:, S], Gfull[S], z[:, S])
+    got = J2[f][np.ix_(jcol, icol)]
+    assert np.linalg.norm(got - ref) <= 1e-7 * np.linalg.norm(ref)
