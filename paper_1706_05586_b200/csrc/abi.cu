@@ -517,11 +517,8 @@ struct NcclApi {
 };
 
 // NCCL is loaded on first use (libnccl.so.2: the one torch already loaded, else the system one)
-NcclApi& nccl_api() {
-    static NcclApi api;
-    static bool tried = false;
-    if (tried) return api;
-    tried = true;
+static NcclApi load_nccl_api() {
+    NcclApi api;
     void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) {
         api.why = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
@@ -544,6 +541,11 @@ NcclApi& nccl_api() {
     api.errStr = reinterpret_cast<decltype(api.errStr)>(sym("ncclGetErrorString"));
     api.ok = ok;
     if (!ok) api.why = "libnccl.so.2 lacks a required symbol";
+    return api;
+}
+
+NcclApi& nccl_api() {
+    static NcclApi api = load_nccl_api();     // thread-safe one-time load
     return api;
 }
 

@@ -605,20 +605,7 @@ static void launch_pass_impl(const PassArgs& a, int nb, cudaStream_t s) {
     if (a.op.nx == GX && a.tl.TY == GT && a.tl.nslots == GS && a.tl.rpt == GR) k = cocg_pass_kernel<FX, GX, GT, GS, GR>;
     DOT_COCG_GEOMS(DOT_PICK)
 #undef DOT_PICK
-    static std::vector<std::pair<K, size_t>> attr;
-    bool found = false;
-    for (auto& e : attr)
-        if (e.first == k) {
-            found = true;
-            if (e.second < a.tl.smem) {
-                DOT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.tl.smem));
-                e.second = a.tl.smem;
-            }
-        }
-    if (!found) {
-        DOT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.tl.smem));
-        attr.emplace_back(k, a.tl.smem);
-    }
+    ensure_smem(k, a.tl.smem);
     dim3 grid(a.tl.ntiles, nb);
     launch_clustered(k, grid, a.tl.threads, a.tl.smem, s, a.tl.cluster, a);
 }

@@ -493,12 +493,7 @@ void launch_z_ns(const PassArgs& a, int nb, cudaStream_t s) {
                        : cocg_zpass_kernel<FX, MAXT, MINB, NS, true, RPT, false>)
                  : (zc ? cocg_zpass_kernel<FX, MAXT, MINB, NS, false, RPT, true>
                        : cocg_zpass_kernel<FX, MAXT, MINB, NS, false, RPT, false>);
-    static size_t attr[4] = {0, 0, 0, 0};
-    const int ai = (mut ? 1 : 0) + (zc ? 2 : 0);
-    if (attr[ai] < a.tl.smem) {
-        DOT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.tl.smem));
-        attr[ai] = a.tl.smem;
-    }
+    ensure_smem(k, a.tl.smem);
     dim3 grid(a.tl.ntiles * a.nzch, nb);
     launch_clustered(k, grid, a.tl.threads, a.tl.smem, s, a.nzch == 1 ? a.tl.cluster : 1, a);
 }

@@ -153,11 +153,7 @@ void launch_nt(int nb, int K, int ld, int ls, int n_p, const double2* Lam, size_
     const int npairs = ld * ls;
     dim3 grid((npairs + BM / 2 - 1) / (BM / 2), (n_p + 8 * NT - 1) / (8 * NT), nb);
     const size_t smem = (size_t)(2 * BM * AS + 2 * BK * (8 * NT + 4)) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        DOT_CUDA_TRY(cudaFuncSetAttribute(contract_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    ensure_smem(contract_kernel<NT>, smem);
     contract_kernel<NT><<<grid, THREADS, smem, s>>>(K, ld, ls, n_p, Lam, lam_bstride, U, u_bstride, G, J);
     DOT_CUDA_TRY(cudaGetLastError());
 }
@@ -442,12 +438,7 @@ void launch_contract(int nb, int K, int ld, int ls, int n_p, const double2* Lam,
         // large panels: per (frequency, basis) complex GEMM on the tensor pipe
         dim3 grid((ld + GTM - 1) / GTM, (5 * ls + GTN - 1) / GTN, sp->n_rbf * nb);
         const size_t smem = (size_t)8 * GTM * GKS * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
-            DOT_CUDA_TRY(cudaFuncSetAttribute(contract_gemm_sparse_kernel,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
-        }
+        ensure_smem(contract_gemm_sparse_kernel, smem);
         contract_gemm_sparse_kernel<<<grid, THREADS, smem, s>>>(K, ld, ls, n_p, sp->n_rbf, Lam, lam_bstride, U,
                                                                 u_bstride, G, sp->seg, sp->segoff, J);
         DOT_CUDA_TRY(cudaGetLastError());
@@ -456,12 +447,7 @@ void launch_contract(int nb, int K, int ld, int ls, int n_p, const double2* Lam,
     if (sp && sp->seg && sp->n_rbf * 5 == n_p) {
         dim3 grid((npairs + BM / 2 - 1) / (BM / 2), sp->n_rbf, nb);
         const size_t smem = (size_t)(2 * BM * SAS + 2 * SBK * SGS) * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
-            DOT_CUDA_TRY(cudaFuncSetAttribute(contract_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)smem));
-            attr = true;
-        }
+        ensure_smem(contract_sparse_kernel, smem);
         contract_sparse_kernel<<<grid, THREADS, smem, s>>>(K, ld, ls, n_p, Lam, lam_bstride, U, u_bstride, G, sp->seg,
                                                            sp->segoff, J);
         DOT_CUDA_TRY(cudaGetLastError());

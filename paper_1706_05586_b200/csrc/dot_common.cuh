@@ -3,7 +3,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "dot_b200.h"   // -I include
@@ -23,6 +26,23 @@ struct Error {
     std::string msg;
     Error(int c, std::string m) : code(c), msg(std::move(m)) {}
 };
+
+// Raise a kernel's dynamic shared-memory limit to at least `smem` on the current device.
+// The attribute is per device, so the record of what was set is keyed by (kernel, device);
+// thread-safe (problems may live on several devices / host threads of one process).
+template <class K>
+void ensure_smem(K kernel, size_t smem) {
+    static std::mutex mtx;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    int dev = 0;
+    DOT_CUDA_TRY(cudaGetDevice(&dev));
+    const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
+    std::lock_guard<std::mutex> lock(mtx);
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= smem) return;
+    DOT_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    done[key] = smem;
+}
 
 // ------------------------------------------------------------------ complex fp64
 __host__ __device__ __forceinline__ double2 cmk(double re, double im) { return make_double2(re, im); }
