@@ -83,6 +83,8 @@ for rep, name in (("prof_pass", "cocg_zpass"), ("prof_contract", "contract")):
 if traffic:
     json.dump(traffic, open(os.path.join(P, "cocg_pass_traffic.json"), "w"), indent=1)
     print(traffic)
+if os.path.exists(os.path.join(G, "sass_mix.txt")):
+    shutil.copy(os.path.join(G, "sass_mix.txt"), os.path.join(P, f"{tag}_ncu_cocg_zpass_sass_mix.txt"))
 bl = [l for l in open(os.path.join(G, "bench.log")) if l.startswith("{")]
 if bl:
     open(os.path.join(P, f"{tag}_bench.jsonl"), "w").write(bl[-1])
