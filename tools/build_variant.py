@@ -1,6 +1,7 @@
 """Build an experimental variant of the library: the package sources with some files
 replaced, into paper_1706_05586_b200/lib/variants/<name>.so (select with DOT_LIB_PATH).
-  python tools/build_variant.py NAME [csrc_file=replacement_path ...]"""
+  python tools/build_variant.py NAME [csrc_file=replacement_path ...]
+(NVCC_EXTRA="flags" adds compiler flags, e.g. ptxas options.)"""
 import os, shutil, subprocess, sys, tempfile
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -20,7 +21,7 @@ for s in sorted(os.listdir(src)):
         continue
     o = os.path.join(tmp, s + ".o")
     cmd = [b.NVCC, *b.ARCH, "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
-           "-c", os.path.join(src, s), "-o", o]
+           *os.environ.get("NVCC_EXTRA", "").split(), "-c", os.path.join(src, s), "-o", o]
     procs.append(subprocess.Popen(cmd))
     objs.append(o)
 assert all(p.wait() == 0 for p in procs)
