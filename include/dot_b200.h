@@ -76,20 +76,24 @@ typedef struct dot_config {
 } dot_config;
 
 typedef struct dot_stats {
-    int64_t rhs_solved;          /* PDE solves performed since create (Table 4 accounting) */
-    int64_t rhs_iterations;      /* sum over solved RHS of COCG iterations                */
+    int64_t rhs_solved;          /* PDE systems A(p, omega_f) x = b solved since create, one per
+                                    (right-hand side, frequency) (Table 4 accounting) */
+    int64_t rhs_iterations;      /* sum over solved systems of the Krylov iterations they took */
     int32_t last_max_iters;      /* max iterations of the last batched solve              */
     int32_t last_min_iters;
     int64_t kernel_launches;     /* kernels launched by the library since create          */
-    int64_t pass_launches;       /* fused COCG pass launches since create                 */
-    double pass_ms;              /* device time in COCG pass kernels (when timing enabled) */
-    double pass_bytes;           /* algorithmic HBM bytes of those passes: 64 B x N x (active RHS) per pass */
+    int64_t pass_launches;       /* fused CG pass launches since create                   */
+    double pass_ms;              /* device time in CG pass kernels (when timing enabled)  */
+    double pass_bytes;           /* algorithmic HBM bytes of those passes: 32 B x N per real seed
+                                    per iteration (read r, p; write r, p in fp64)            */
     double contract_ms;          /* device time in the Jacobian contraction (timing enabled) */
     double contract_flops;       /* its useful flops: 4 x pairs x (points, parameter) pairs with a
                                     nonzero dA/dp block (block-sparse by basis, L972)            */
     int32_t support_K;           /* |S|: nodes where dA/dp != 0 after the last set_params */
     int32_t n_samples;           /* |P| = |S u detectors u sources|: nodes where solutions are kept */
     double contract_flops_dense; /* the dense-equivalent flops 4 x pairs x K x n_p of the same calls */
+    int64_t seeds_solved;        /* real multi-shift CG seeds run (one serves every frequency)   */
+    int64_t seed_iterations;     /* sum over seeds of their iterations                           */
 } dot_stats;
 
 const char* dot_version(void);
@@ -181,25 +185,45 @@ int dot_optimize_directions_subspace(dot_problem* P, int32_t k, int32_t iters, i
  * with NCCL halo exchange and an allreduce of Krylov inner products in the few-
  * simultaneous-source regime").  Rank r of `world`
  * owns a contiguous range of z chunks and iterates only those planes (plus the halo
- * planes it recomputes); after every COCG pass the two boundary planes of r_{k+1}
- * and p_k go to the neighbours and the per-chunk partial sums of the Krylov inner
- * products are all-reduced, so all ranks take identical steps.  Sampled solutions
- * are all-reduced at the end and land in each rank's field caches, after which
- * dot_misfit / dot_jacobian / dot_solve_sampled on any rank use them without solves.
+ * planes it recomputes); after every CG pass the two boundary planes of r_{k+1} and
+ * p_k of every seed pair are packed into ONE buffer per neighbour, exchanged, and the
+ * per-chunk partial sums of the Krylov inner products are summed over the ranks, so
+ * all ranks take identical steps.  Each rank folds the shifted solutions on its own
+ * samples; they are summed over the ranks at the end and land in each rank's field
+ * caches, after which dot_misfit / dot_jacobian / dot_solve_sampled on any rank use
+ * them without solves.
+ *
+ * Three transports, one code path:
+ *  - all ranks in this process (nlocal == world): device copies (single-GPU emulation);
+ *  - one rank per process with NCCL (nlocal == 1, nccl_id): ncclSend/ncclRecv of the
+ *    packed halo buffers, ncclAllReduce of the partials;
+ *  - one rank per process with a caller transport (dot_dd_create_transport): the packed
+ *    buffers are staged through host memory and handed to the caller's callbacks, e.g.
+ *    torch.distributed point-to-point and all_reduce over a gloo group.
  *
  * dot_nccl_unique_id: 128-byte NCCL id (host); rank 0 creates it, the caller
  *   broadcasts it (e.g. torch.distributed).  NCCL is loaded at run time.
  * dot_dd_create: `local` [nlocal] problems of ranks rank0 .. rank0+nlocal-1.  Either
- *   nlocal == world (all ranks in this process, exchanged with device copies -- the
- *   single-GPU emulation) or nlocal == 1 with nccl_id (one rank per process / GPU).
- *   All ranks hold the same problem and parameters (dot_set_params on each).
+ *   nlocal == world or nlocal == 1 with nccl_id.  All ranks hold the same problem and
+ *   parameters (dot_set_params on each).
+ * dot_transport: sendrecv(ctx, peer, send, send_bytes, recv, recv_bytes) exchanges host
+ *   buffers with rank `peer` (the peer calls it with the mirrored sizes; either size may be
+ *   0); allreduce_sum(ctx, buf, n) sums n doubles in place over all ranks.  Both return 0
+ *   on success.  Called on the thread that called dot_dd_fields, buffers owned by the
+ *   library and valid for the duration of the call.
  * dot_dd_fields: solve the forward fields of B W (ls columns; W NULL = identity;
  *   ls = 0: none) and the adjoint fields of C V (ld; likewise) for every frequency
  *   in one decomposed batch and cache them on every local rank.  Errors as
- *   dot_misfit; DOT_ERR_ARG if nz < 2 * world. */
+ *   dot_misfit; DOT_ERR_ARG if nz < 2 * world; DOT_ERR_CUDA if a transport call fails. */
+typedef struct dot_transport {
+    void* ctx;
+    int (*sendrecv)(void* ctx, int32_t peer, const void* send, size_t send_bytes, void* recv, size_t recv_bytes);
+    int (*allreduce_sum)(void* ctx, double* buf, size_t n);
+} dot_transport;
 int dot_nccl_unique_id(unsigned char* id_out);
 int dot_dd_create(dot_problem* const* local, int32_t nlocal, int32_t rank0, int32_t world,
                   const unsigned char* nccl_id, dot_dd** out);
+int dot_dd_create_transport(dot_problem* local, int32_t rank, int32_t world, const dot_transport* t, dot_dd** out);
 int dot_dd_fields(dot_dd* G, const double* W, int32_t ls, const double* V, int32_t ld, int where);
 const char* dot_dd_last_error(const dot_dd* G);
 int dot_dd_destroy(dot_dd* G);

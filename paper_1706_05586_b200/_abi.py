@@ -38,6 +38,7 @@ class DotStats(C.Structure):
         ("contract_ms", C.c_double), ("contract_flops", C.c_double),
         ("support_K", C.c_int32), ("n_samples", C.c_int32),
         ("contract_flops_dense", C.c_double),
+        ("seeds_solved", C.c_int64), ("seed_iterations", C.c_int64),
     ]
 
     def as_dict(self):

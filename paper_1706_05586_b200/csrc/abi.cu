@@ -25,7 +25,8 @@ struct FieldCache {
     int ncols = 0;
     std::vector<double> coeff;        // [n_side][ncols] host copy (empty for identity)
     std::vector<int> sel;             // cached columns are the point sources sel[j] (selection / identity)
-    DBuf<double2> X;                  // [n_freq][ncols][nP]
+    std::shared_ptr<DBuf<double2>> blk;   // the solve's output block (shared by the sides solved together)
+    double2* X = nullptr;             // [n_freq][ncols][nP] inside blk
 };
 
 struct dot_problem {
@@ -39,7 +40,7 @@ struct dot_problem {
     std::vector<int32_t> src, det;
     std::vector<double> src_scale, det_scale;
     OpConst op{};
-    CocgTiling tl{};
+    CgTiling tl{};
     PalsConst pc{};
     cudaStream_t stream = nullptr;
     std::string err;
@@ -134,85 +135,105 @@ std::vector<double> host_copy(dot_problem* P, const double* src, size_t count, i
     return h;
 }
 
-size_t per_rhs_bytes(const dot_problem* P) {
+// device bytes per pair of seeds iterated together (r, p ping-pong; history, shifted state
+// on the samples; partial slots; states)
+// hist: passes between folds (history ring depth); nsl: shifts kept per seed
+size_t per_pair_bytes(const dot_problem* P, int nP, int hist, int nsl) {
     const size_t vec = P->N * sizeof(double2);
     const size_t zmax = (size_t)std::max(1, P->nz / 4);
-    return 4 * vec + 2 * P->tl.ntiles * zmax * kNumPartials * sizeof(double) + 2 * sizeof(RhsState) +
-           sizeof(double) + 4 * Arena::kAlign;
+    const size_t samp = (size_t)std::max(nP, 1) * sizeof(double2) * ((size_t)hist + 4 * (size_t)nsl);
+    return 4 * vec + samp + 2 * P->tl.ntiles * zmax * kNumPartials * sizeof(double) +
+           4 * sizeof(SeedState) + 4 * kMaxShift * sizeof(ShiftState) + 2 * hist * kMaxShift * sizeof(ShiftCoef) +
+           8 * sizeof(int32_t) + 10 * Arena::kAlign;
 }
 
 // ---------------------------------------------------------------- batched solve
-// Solve the global RHS list r = f*ncols + c, f < n_freq, c < ncols, where RHS
-// (f, c) is either the point-combination `side` (0: B coeff[:,c], 1: C coeff[:,c])
-// or, if dense != null, the dense vector dense[r].  Outputs: XP [n_rhs][nP]
-// (sampled) or, if Xfull != null, Xfull [n_rhs][N].  freq_of: optional per-RHS
-// frequency (dense mode).  Returns per-RHS iterations.
 // One segment of point-combination right-hand sides: RHS (f, c) = side's point
-// combination with coefficient column c at frequency f, f-major (nf * ncols RHS).
+// combination with coefficient column c at frequency f, f-major (nf * ncols outputs).
 struct Seg {
     int side;
     const double* d_coeff;   // device [n_side][ncols] or null (identity)
     int ncols;
 };
 
-std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, int n_rhs, const double2* dense,
-                                 const int32_t* d_freq_of, double2* XP, double2* Xfull);
+// Seeds of a batch: point mode -- one real seed per column c of each
+// segment, delivering all n_freq shifts, output (f, c) of the segment; dense mode -- the
+// complex RHS r is the seed pair (Re, Im) at its own frequency only.
+struct SeedPlan {
+    int nseeds = 0;                  // even (a dummy seed pads an odd count)
+    std::vector<uint32_t> mask;      // needed shifts
+    std::vector<int32_t> omap;       // 3 per seed: output base, stride per shift, imaginary part
+    std::vector<int32_t> seg, col;   // point mode: segment and column (-1: dummy)
+};
 
-std::vector<int32_t> solve_rhs(dot_problem* P, int side, const double* d_coeff, int ncols, int n_rhs,
-                               const double2* dense, const int32_t* d_freq_of, double2* XP,
-                               double2* Xfull) {
-    std::vector<Seg> segs;
-    if (!dense) segs.push_back(Seg{side, d_coeff, ncols});
-    return solve_batch(P, segs, n_rhs, dense, d_freq_of, XP, Xfull);
-}
-
-// R0 [nb][N] and shift [nb] of global RHS r0 .. r0+nb-1 of the concatenated segments.
-void build_point_rhs(dot_problem* P, const std::vector<Seg>& segs, long long r0, int nb, double2* R0, double* shift) {
-    const size_t N = P->N;
-    DOT_CUDA_TRY(cudaMemsetAsync(R0, 0, (size_t)nb * N * sizeof(double2), P->stream));
-    long long gs = 0;
-    for (const Seg& sg : segs) {                 // the part of each segment inside [r0, r0 + nb)
-        const long long ge = gs + (long long)P->n_freq * sg.ncols;
-        const long long rs = std::max<long long>(r0, gs), re = std::min<long long>(r0 + nb, ge);
-        if (rs < re) {
-            const int nn = sg.side == 0 ? P->n_src : P->n_det;
-            launch_scatter_rhs(R0 + (size_t)(rs - r0) * N, N, (int)(re - rs), rs - gs, sg.ncols,
-                               sg.side == 0 ? P->d_src.get() : P->d_det.get(), nn, sg.d_coeff,
-                               sg.side == 0 ? P->d_src_scale.get() : P->d_det_scale.get(), P->stream);
-            launch_fill_shift(shift + (rs - r0), (int)(re - rs), rs - gs, sg.ncols, P->d_omega_nu.get(), P->stream);
-            P->stats.kernel_launches += 2;
+SeedPlan plan_point(const dot_problem* P, const std::vector<Seg>& segs) {
+    SeedPlan sp;
+    const uint32_t all = P->n_freq >= 32 ? 0xffffffffu : ((1u << P->n_freq) - 1u);
+    int base = 0;
+    for (int g = 0; g < (int)segs.size(); ++g) {
+        for (int c = 0; c < segs[g].ncols; ++c) {
+            sp.mask.push_back(all);
+            sp.omap.insert(sp.omap.end(), {base + c, segs[g].ncols, 0});
+            sp.seg.push_back(g);
+            sp.col.push_back(c);
         }
-        gs = ge;
+        base += P->n_freq * segs[g].ncols;
     }
+    if (sp.mask.size() % 2) {
+        sp.mask.push_back(0);
+        sp.omap.insert(sp.omap.end(), {-1, 0, 0});
+        sp.seg.push_back(-1);
+        sp.col.push_back(-1);
+    }
+    sp.nseeds = (int)sp.mask.size();
+    return sp;
 }
 
-// Batched solve of the concatenated RHS lists of `segs` (point mode) or of the dense
-// vectors `dense` (with per-RHS frequency d_freq_of).  All RHS iterate together in
-// chunks of what fits the workspace.
-std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, int n_rhs, const double2* dense,
-                                 const int32_t* d_freq_of, double2* XP, double2* Xfull) {
-    std::vector<int32_t> iters(n_rhs, 0);
-    if (n_rhs == 0) return iters;
+SeedPlan plan_dense(const dot_problem* P, const std::vector<int32_t>& freq_of) {
+    SeedPlan sp;
+    for (int r = 0; r < (int)freq_of.size(); ++r) {
+        if (freq_of[r] < 0 || freq_of[r] >= P->n_freq) throw Error(DOT_ERR_ARG, "frequency index out of range");
+        for (int e = 0; e < 2; ++e) {
+            sp.mask.push_back(1u << freq_of[r]);
+            sp.omap.insert(sp.omap.end(), {r, 0, e});
+            sp.seg.push_back(-1);
+            sp.col.push_back(-1);
+        }
+    }
+    sp.nseeds = (int)sp.mask.size();
+    return sp;
+}
+
+// Batched multi-shift solve.  Outputs XP [n_out][nP_out] on the sample list (samp_nodes,
+// samp_off; the problem's P, or every node for dense solutions).  Point mode: segs;
+// dense mode: dense [n_rhs][N] complex with host frequency list freq_of.  Returns per-output
+// seed iterations (dense mode).
+std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, const double2* dense,
+                                 const std::vector<int32_t>& freq_of, double2* XP, int n_out, int nP_out,
+                                 const int32_t* samp_nodes, const int32_t* samp_off) {
+    const SeedPlan sp = dense ? plan_dense(P, freq_of) : plan_point(P, segs);
+    std::vector<int32_t> iters(n_out, 0);
+    if (sp.nseeds == 0) return iters;
+    if (P->n_freq > kMaxShift) throw Error(DOT_ERR_ARG, "more frequencies than the solver's shift capacity (8)");
     const size_t N = P->N;
-    const size_t prb = per_rhs_bytes(P);
-    size_t fit = P->arena.largest_free() / prb;
-    // multiple allocations fragment the arena: keep a safety margin
-    fit = fit > 2 ? fit - 1 : fit;
-    if (fit < 1) throw Error(DOT_ERR_WORKSPACE, "workspace too small for one right-hand side");
-    const int chunk = (int)std::min<size_t>(fit, (size_t)n_rhs);
+    const int nf = P->n_freq, nP = nP_out;
+    const int npairs = sp.nseeds / 2;
+    const int hist = dense ? 8 : kHist;      // dense solutions sample every node: fold every poll group
+    const int nsl = dense ? 1 : nf;
+    const size_t ppb = per_pair_bytes(P, nP, hist, nsl);
+    size_t fit = P->arena.largest_free() / ppb;
+    fit = fit > 2 ? fit - 1 : fit;      // several allocations fragment the arena: keep a margin
+    if (fit < 1) throw Error(DOT_ERR_WORKSPACE, "workspace too small for one pair of right-hand sides");
+    const int chunk = (int)std::min<size_t>(fit, (size_t)npairs);
     const int CHK = 8;
-    // z chunks (z pass): enough CTAs to fill the GPU when few RHS iterate together on a
-    // deep grid; at least 8 planes per chunk.  DOT_COCG_ZCHUNKS overrides.
+    // z chunks: enough CTAs to fill the GPU when few pairs iterate together on a deep grid
+    // (DESIGN.md "z chunks"); at least 8 planes per chunk.  DOT_CG_ZCHUNKS overrides.
     auto zchunks = [&](int nb) {
-        if (P->tl.kind != 1) return 1;
         int n = 1;
-        const char* e = std::getenv("DOT_COCG_ZCHUNKS");
+        const char* e = std::getenv("DOT_CG_ZCHUNKS");
         if (e) {
             n = std::min(std::max(1, std::atoi(e)), std::max(1, P->nz / 4));
         } else {
-            // measured (tools/rowsweep.sh): chunks pay off on deep grids (opt96, 96^3: 94 -> 110
-            // RHS solves/s) but not on shallow ones, where a chunk's halo planes and CTA start-up
-            // dominate (sketch32, 32^3: 4 chunks 3720 vs none 4180)
             const long long target = 4LL * P->num_sms;
             const long long have = (long long)P->tl.ntiles * nb;
             if (have < target && P->nz >= 64) n = (int)((target + have - 1) / have);
@@ -221,86 +242,120 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, i
         const int zlen = (P->nz + n - 1) / n;
         return (P->nz + zlen - 1) / zlen;
     };
-
-    for (int r0 = 0; r0 < n_rhs; r0 += chunk) {
-        const int nb = std::min(chunk, n_rhs - r0);
+    DOT_CUDA_TRY(cudaMemsetAsync(XP, 0, (size_t)n_out * nP * sizeof(double2), P->stream));
+    int mx = 0, mn = 1 << 30;
+    for (int p0 = 0; p0 < npairs; p0 += chunk) {
+        const int nb = std::min(chunk, npairs - p0);
+        const int s0 = 2 * p0, ns = 2 * nb;               // seeds of this chunk
         DBuf<double2> R0(P->arena, nb * N), R1(P->arena, nb * N), P0(P->arena, nb * N), P1(P->arena, nb * N);
         const int nzch = zchunks(nb);
-        DBuf<double> part(P->arena, 2 * (size_t)nb * P->tl.ntiles * nzch * kNumPartials);
-        DBuf<RhsState> st(P->arena, 2 * (size_t)nb);
-        DBuf<double> shift(P->arena, nb);
-        DBuf<int32_t> act(P->arena, nb);                 // active-RHS list of the tail passes
+        const size_t nslot = (size_t)P->tl.ntiles * nzch;
+        DBuf<double> part(P->arena, 2 * (size_t)nb * nslot * kNumPartials);
+        DBuf<SeedState> st(P->arena, 2 * (size_t)ns);
+        DBuf<ShiftState> shs(P->arena, 2 * (size_t)ns * kMaxShift);
+        DBuf<ShiftCoef> coef(P->arena, (size_t)hist * ns * kMaxShift);
+        DBuf<double2> H(P->arena, (size_t)hist * nb * std::max(nP, 1));
+        DBuf<double2> Ps(P->arena, (size_t)ns * nsl * std::max(nP, 1)), Xs(P->arena, (size_t)ns * nsl * std::max(nP, 1));
+        DBuf<int32_t> act(P->arena, nb);
+        DBuf<uint32_t> dmask = to_device(P, sp.mask.data() + s0, ns, DOT_HOST);
+        DBuf<int32_t> domap = to_device(P, sp.omap.data() + 3 * s0, 3 * ns, DOT_HOST);
         int nb_launch = nb;
+        DOT_CUDA_TRY(cudaMemsetAsync(coef.get(), 0, (size_t)hist * ns * kMaxShift * sizeof(ShiftCoef), P->stream));
+        DOT_CUDA_TRY(cudaMemsetAsync(Ps.get(), 0, (size_t)ns * nsl * std::max(nP, 1) * sizeof(double2), P->stream));
+        DOT_CUDA_TRY(cudaMemsetAsync(Xs.get(), 0, (size_t)ns * nsl * std::max(nP, 1) * sizeof(double2), P->stream));
 
-        // ---- right-hand sides
+        // ---- right-hand sides of the seeds (scaled by theta^-1/2)
         if (dense) {
-            DOT_CUDA_TRY(cudaMemcpyAsync(R0.get(), dense + (size_t)r0 * N, (size_t)nb * N * sizeof(double2),
-                                         cudaMemcpyDeviceToDevice, P->stream));
+            launch_split_dense(R0.get(), dense + (size_t)p0 * N, N, nb, P->op, P->stream);
+            P->stats.kernel_launches++;
         } else {
-            build_point_rhs(P, segs, r0, nb, R0.get(), shift.get());
-        }
-        if (d_freq_of) {
-            // shift[r] = omega_nu[freq_of[r0 + r]] : reuse fill_shift with ncols = 1 on a gathered table
-            std::vector<int32_t> fh(nb);
-            DOT_CUDA_TRY(cudaMemcpyAsync(fh.data(), d_freq_of + r0, nb * sizeof(int32_t), cudaMemcpyDeviceToHost,
-                                         P->stream));
-            sync(P);
-            std::vector<double> sh(nb);
-            for (int r = 0; r < nb; ++r) {
-                if (fh[r] < 0 || fh[r] >= P->n_freq) throw Error(DOT_ERR_ARG, "frequency index out of range");
-                sh[r] = P->omega[fh[r]] / P->nu;
+            DOT_CUDA_TRY(cudaMemsetAsync(R0.get(), 0, (size_t)nb * N * sizeof(double2), P->stream));
+            for (int q = s0; q < s0 + ns;) {           // runs of consecutive columns of one segment
+                const int g = sp.seg[q];
+                int e = q + 1;
+                while (e < s0 + ns && sp.seg[e] == g && sp.col[e] == sp.col[e - 1] + 1) ++e;
+                if (g >= 0) {
+                    const Seg& sg = segs[g];
+                    launch_scatter_seeds(R0.get(), N, sg.side == 0 ? P->d_src.get() : P->d_det.get(),
+                                         sg.side == 0 ? P->n_src : P->n_det, sg.d_coeff, sg.ncols,
+                                         sg.side == 0 ? P->d_src_scale.get() : P->d_det_scale.get(), sp.col[q],
+                                         q - s0, e - q, P->op, P->stream);
+                    P->stats.kernel_launches++;
+                }
+                q = e;
             }
-            DOT_CUDA_TRY(cudaMemcpyAsync(shift.get(), sh.data(), nb * sizeof(double), cudaMemcpyHostToDevice,
-                                         P->stream));
-            sync(P);
         }
-        if (XP) DOT_CUDA_TRY(cudaMemsetAsync(XP + (size_t)r0 * P->nP, 0, (size_t)nb * P->nP * sizeof(double2), P->stream));
-        if (Xfull) DOT_CUDA_TRY(cudaMemsetAsync(Xfull + (size_t)r0 * N, 0, (size_t)nb * N * sizeof(double2), P->stream));
 
         PassArgs a;
         a.op = P->op;
         a.tl = P->tl;
         a.max_iter = P->max_iter;
         a.tol2 = P->tol * P->tol;
+        a.nshift = nf;
+        for (int f = 0; f < nf; ++f) a.sigma[f] = P->omega[f] / P->nu;
         a.mu = P->d_mu.get();
-        a.shift = shift.get();
         a.R[0] = R0.get();
         a.R[1] = R1.get();
         a.Pv[0] = P0.get();
         a.Pv[1] = P1.get();
         a.part[0] = part.get();
-        a.part[1] = part.get() + (size_t)nb * P->tl.ntiles * nzch * kNumPartials;
+        a.part[1] = part.get() + (size_t)nb * nslot * kNumPartials;
         a.nzch = nzch;
         a.nzch_tot = nzch;
         a.zc0 = 0;
         a.zlen = (P->nz + nzch - 1) / nzch;
         a.st[0] = st.get();
-        a.st[1] = st.get() + nb;
-        a.samp_nodes = P->d_P.get();
-        a.samp_off = P->d_off.get();
-        a.XP = XP ? XP + (size_t)r0 * P->nP : nullptr;
-        a.nP = XP ? P->nP : 0;
-        a.X = Xfull ? Xfull + (size_t)r0 * N : nullptr;
+        a.st[1] = st.get() + ns;
+        a.sh[0] = shs.get();
+        a.sh[1] = shs.get() + (size_t)ns * kMaxShift;
+        a.mask = dmask.get();
+        a.coef = coef.get();
+        a.hist = hist;
+        a.npairs = nb;
+        a.samp_nodes = samp_nodes;
+        a.samp_off = samp_off;
+        a.nP = nP;
+        a.H = H.get();
+        FoldArgs fa;
+        fa.s0 = 0;
+        fa.s1 = nP;
+        fa.npairs = nb;
+        fa.nshift = nf;
+        fa.hist = hist;
+        fa.nsl = nsl;
+        fa.nP = std::max(nP, 1);
+        fa.mask = dmask.get();
+        fa.coef = coef.get();
+        fa.H = H.get();
+        fa.Ps = Ps.get();
+        fa.Xs = Xs.get();
 
-        launch_cocg_init(a, nb, P->stream);
+        launch_cg_init(a, nb, P->stream);
         P->stats.kernel_launches++;
         // Groups of CHK passes; each ends with a convergence count into pinned memory.  The
         // poll is pipelined: group g+1 is enqueued before the host reads group g-1's count,
         // so the GPU never idles on the host round trip (a group launched after the last
-        // RHS finished runs as no-ops).
-        int k = 0, g = 0;
+        // pair finished runs as no-ops).  Every kHist passes the fold kernel applies the
+        // shifted recurrences of those passes on the samples.
+        int k = 0, g = 0, kf = 0;
         size_t ev = 0;
         for (;;) {
             if (P->timing) DOT_CUDA_TRY(cudaEventRecord(event_at(P, ev++), P->stream));
             for (int i = 0; i < CHK; ++i) {
                 a.k = k++;
-                launch_cocg_pass(a, nb_launch, P->stream);
+                launch_cg_pass(a, nb_launch, P->stream);
                 P->stats.kernel_launches++;
                 P->stats.pass_launches++;
             }
             if (P->timing) DOT_CUDA_TRY(cudaEventRecord(event_at(P, ev++), P->stream));
-            launch_count_active(a.st[(k - 1) & 1], nb, P->d_count.get() + (g & 1), P->stream,
-                                P->tl.kind == 1 ? act.get() : nullptr);
+            if (k - kf >= hist) {
+                fa.k0 = kf;
+                fa.k1 = k;
+                launch_cg_fold(fa, P->stream);
+                P->stats.kernel_launches++;
+                kf = k;
+            }
+            launch_count_active(a.st[(k - 1) & 1], nb, P->d_count.get() + (g & 1), P->stream, act.get());
             P->stats.kernel_launches++;
             DOT_CUDA_TRY(cudaMemcpyAsync(P->h_count + (g & 1), P->d_count.get() + (g & 1), sizeof(int),
                                          cudaMemcpyDeviceToHost, P->stream));
@@ -309,13 +364,16 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, i
                 DOT_CUDA_TRY(cudaEventSynchronize(P->poll_ev[(g - 1) & 1]));
                 const int c = P->h_count[(g - 1) & 1];
                 if (c == 0) break;
-                if (P->tl.kind == 1) {     // later passes launch only the RHS still iterating
-                    a.act = act.get();
-                    nb_launch = c;
-                }
+                a.act = act.get();      // later passes launch only the pairs still iterating
+                nb_launch = c;
             }
             ++g;
         }
+        fa.k0 = kf;
+        fa.k1 = k;
+        launch_cg_fold(fa, P->stream);
+        launch_cg_finalize(fa, P->op, XP, nP, domap.get(), samp_nodes, P->stream);
+        P->stats.kernel_launches += 2;
         sync(P);
         if (P->timing) {
             for (size_t e = 0; e + 1 < ev; e += 2) {
@@ -324,28 +382,35 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, i
                 P->stats.pass_ms += ms;
             }
         }
-        std::vector<RhsState> hs(nb);
-        DOT_CUDA_TRY(cudaMemcpyAsync(hs.data(), a.st[(k - 1) & 1], nb * sizeof(RhsState), cudaMemcpyDeviceToHost,
+        std::vector<SeedState> hs(ns);
+        DOT_CUDA_TRY(cudaMemcpyAsync(hs.data(), a.st[(k - 1) & 1], ns * sizeof(SeedState), cudaMemcpyDeviceToHost,
                                      P->stream));
         sync(P);
-        int mx = 0, mn = 1 << 30;
-        for (int r = 0; r < nb; ++r) {
-            if (hs[r].flag == DOT_ERR_NOCONV)
-                throw Error(DOT_ERR_NOCONV, "COCG did not converge within max_iter for rhs " + std::to_string(r0 + r));
-            if (hs[r].flag == DOT_ERR_BREAKDOWN)
-                throw Error(DOT_ERR_BREAKDOWN, "COCG breakdown for rhs " + std::to_string(r0 + r) + " at iteration " +
-                                                   std::to_string(hs[r].iters) + " (batch of " + std::to_string(nb) +
-                                                   ", chunk start " + std::to_string(r0) + ")");
-            iters[r0 + r] = hs[r].iters;
-            mx = std::max(mx, hs[r].iters);
-            mn = std::min(mn, hs[r].iters);
-            P->stats.rhs_iterations += hs[r].iters;
-            P->stats.pass_bytes += 64.0 * (double)N * hs[r].iters;
+        for (int q = 0; q < ns; ++q) {
+            const int seed = s0 + q;
+            if (!sp.mask[seed]) continue;
+            if (hs[q].flag == DOT_ERR_NOCONV)
+                throw Error(DOT_ERR_NOCONV, "CG did not converge within max_iter for seed " + std::to_string(seed));
+            if (hs[q].flag == DOT_ERR_BREAKDOWN)
+                throw Error(DOT_ERR_BREAKDOWN, "CG breakdown for seed " + std::to_string(seed) + " at iteration " +
+                                                   std::to_string(hs[q].iters));
+            const int it = hs[q].iters;
+            const int systems = dense ? (sp.omap[3 * seed + 2] ? 0 : 1) : __builtin_popcount(sp.mask[seed]);
+            if (dense) {
+                int& o = iters[sp.omap[3 * seed]];
+                o = std::max(o, it);
+            }
+            P->stats.seeds_solved++;
+            P->stats.seed_iterations += it;
+            P->stats.rhs_solved += systems;
+            P->stats.rhs_iterations += (int64_t)systems * it;
+            P->stats.pass_bytes += 32.0 * (double)N * it;
+            mx = std::max(mx, it);
+            mn = std::min(mn, it);
         }
-        P->stats.rhs_solved += nb;
-        P->stats.last_max_iters = mx;
-        P->stats.last_min_iters = mn;
     }
+    P->stats.last_max_iters = mx;
+    P->stats.last_min_iters = mn;
     return iters;
 }
 
@@ -391,18 +456,21 @@ void solve_and_cache(dot_problem* P, const std::vector<Req>& reqs) {
         total += P->n_freq * q.ncols;
     }
     const size_t nPp = (size_t)std::max(P->nP, 1);
-    DBuf<double2> XPj(P->arena, (size_t)total * nPp);
-    solve_batch(P, segs, total, nullptr, nullptr, XPj.get(), nullptr);
+    for (const Req& q : reqs) {              // the caches being replaced free their memory first
+        FieldCache& c = P->cache[q.side];
+        c.valid = false;
+        c.blk.reset();
+        c.X = nullptr;
+    }
+    auto blk = std::make_shared<DBuf<double2>>(P->arena, (size_t)total * nPp);
+    solve_batch(P, segs, nullptr, {}, blk->get(), total, P->nP, P->d_P.get(), P->d_off.get());
     size_t off = 0;
     for (const Req& q : reqs) {
         const int n_side = q.side == 0 ? P->n_src : P->n_det;
         FieldCache& c = P->cache[q.side];
-        c.valid = false;
-        c.X.reset();
         const size_t n = (size_t)P->n_freq * q.ncols * nPp;
-        c.X = DBuf<double2>(P->arena, n);
-        DOT_CUDA_TRY(cudaMemcpyAsync(c.X.get(), XPj.get() + off, n * sizeof(double2), cudaMemcpyDeviceToDevice,
-                                     P->stream));
+        c.blk = blk;
+        c.X = blk->get() + off;
         off += n;
         c.valid = true;
         c.identity = q.identity;
@@ -446,8 +514,8 @@ const double2* get_fields(dot_problem* P, int side, const std::vector<double>& h
     const Req q{side, hc, identity, ncols};
     if (!cache_hit(P, q)) solve_and_cache(P, {q});
     FieldCache& c = P->cache[side];
-    if (identity && c.identity) return c.X.get();
-    if (!identity && !c.identity && c.ncols == ncols && c.coeff == hc) return c.X.get();
+    if (identity && c.identity) return c.X;
+    if (!identity && !c.identity && c.ncols == ncols && c.coeff == hc) return c.X;
     // combination of the cached point sources sel[0..m):
     // X'[f][c][q] = sum_j coeff[sel_j][c] X[f][j][q]
     const int m = (int)c.sel.size();
@@ -456,7 +524,7 @@ const double2* get_fields(dot_problem* P, int side, const std::vector<double>& h
         for (int k = 0; k < ncols; ++k) X[(size_t)j * ncols + k] = hc[(size_t)c.sel[j] * ncols + k];
     DBuf<double> dc = to_device(P, X.data(), X.size(), DOT_HOST);
     tmp = DBuf<double2>(P->arena, (size_t)P->n_freq * ncols * std::max(P->nP, 1));
-    launch_rc_gemm(P->n_freq, ncols, P->nP, m, dc.get(), ncols, c.X.get(), (size_t)m * P->nP, P->nP, 1, tmp.get(),
+    launch_rc_gemm(P->n_freq, ncols, P->nP, m, dc.get(), ncols, c.X, (size_t)m * P->nP, P->nP, 1, tmp.get(),
                    (size_t)ncols * P->nP, P->nP, 1, P->stream);
     P->stats.kernel_launches++;
     sync(P);
@@ -466,7 +534,8 @@ const double2* get_fields(dot_problem* P, int side, const std::vector<double>& h
 void invalidate_caches(dot_problem* P) {
     for (auto& c : P->cache) {
         c.valid = false;
-        c.X.reset();
+        c.blk.reset();
+        c.X = nullptr;
         c.coeff.clear();
         c.sel.clear();
     }
@@ -568,7 +637,9 @@ struct DDPlan {
 struct dot_dd {
     std::vector<dot_problem*> loc;  // local ranks rank0 .. rank0 + loc.size() - 1
     int rank0 = 0, world = 1;
-    ncclComm_t comm = nullptr;      // one local rank per process when set
+    ncclComm_t comm = nullptr;      // one local rank per process, NCCL transport
+    bool host = false;              // one local rank per process, host-staged caller transport
+    dot_transport tr{};
     std::string err;
 };
 
@@ -595,31 +666,128 @@ DDPlan dd_plan(const dot_dd* G, int nb) {
     return pl;
 }
 
+// Exchange step of the decomposition for one rank per process: halo planes with the two
+// neighbours and the in-place sum of the Krylov partials / sampled solutions over all ranks.
+// Buffers are device buffers on `s`.
+struct Transport {
+    virtual ~Transport() = default;
+    // send s_lo (n_lo_s) to rank - 1 and s_hi (n_hi_s) to rank + 1; receive r_lo (n_lo_r) from
+    // rank - 1 and r_hi (n_hi_r) from rank + 1 (counts in double2; 0 = no such neighbour)
+    virtual void halo(const double2* s_lo, size_t n_lo_s, double2* r_lo, size_t n_lo_r, const double2* s_hi,
+                      size_t n_hi_s, double2* r_hi, size_t n_hi_r, cudaStream_t s) = 0;
+    virtual void allreduce(double* buf, size_t n, cudaStream_t s) = 0;
+    virtual bool synchronous() const = 0;
+};
+
+struct NcclTransport : Transport {
+    ncclComm_t comm;
+    int rank;
+    explicit NcclTransport(ncclComm_t c, int r) : comm(c), rank(r) {}
+    void halo(const double2* s_lo, size_t n_lo_s, double2* r_lo, size_t n_lo_r, const double2* s_hi, size_t n_hi_s,
+              double2* r_hi, size_t n_hi_r, cudaStream_t s) override {
+        NcclApi& nc = nccl_api();
+        DOT_NCCL_TRY(nc.groupStart());
+        if (n_hi_s) DOT_NCCL_TRY(nc.send(s_hi, 2 * n_hi_s, ncclDouble, rank + 1, comm, s));
+        if (n_hi_r) DOT_NCCL_TRY(nc.recv(r_hi, 2 * n_hi_r, ncclDouble, rank + 1, comm, s));
+        if (n_lo_s) DOT_NCCL_TRY(nc.send(s_lo, 2 * n_lo_s, ncclDouble, rank - 1, comm, s));
+        if (n_lo_r) DOT_NCCL_TRY(nc.recv(r_lo, 2 * n_lo_r, ncclDouble, rank - 1, comm, s));
+        DOT_NCCL_TRY(nc.groupEnd());
+    }
+    void allreduce(double* buf, size_t n, cudaStream_t s) override {
+        DOT_NCCL_TRY(nccl_api().allReduce(buf, buf, n, ncclDouble, ncclSum, comm, s));
+    }
+    bool synchronous() const override { return false; }
+};
+
+// host-staged exchange through the caller's callbacks (e.g. torch.distributed on gloo)
+struct HostTransport : Transport {
+    dot_transport t;
+    int rank;
+    std::vector<char> a, b;        // staging (pageable; the copies are synchronous here)
+    HostTransport(const dot_transport& tr, int r) : t(tr), rank(r) {}
+    void stage(std::vector<char>& v, size_t bytes) {
+        if (v.size() < bytes) v.resize(bytes);
+    }
+    void one(int peer, const double2* sd, size_t ns, double2* rd, size_t nr, cudaStream_t s) {
+        if (!ns && !nr) return;
+        stage(a, ns * sizeof(double2));
+        stage(b, nr * sizeof(double2));
+        if (ns) DOT_CUDA_TRY(cudaMemcpyAsync(a.data(), sd, ns * sizeof(double2), cudaMemcpyDeviceToHost, s));
+        DOT_CUDA_TRY(cudaStreamSynchronize(s));
+        if (t.sendrecv(t.ctx, peer, a.data(), ns * sizeof(double2), b.data(), nr * sizeof(double2)) != 0)
+            throw Error(DOT_ERR_CUDA, "transport sendrecv failed");
+        if (nr) DOT_CUDA_TRY(cudaMemcpyAsync(rd, b.data(), nr * sizeof(double2), cudaMemcpyHostToDevice, s));
+        DOT_CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    void halo(const double2* s_lo, size_t n_lo_s, double2* r_lo, size_t n_lo_r, const double2* s_hi, size_t n_hi_s,
+              double2* r_hi, size_t n_hi_r, cudaStream_t s) override {
+        one(rank - 1, s_lo, n_lo_s, r_lo, n_lo_r, s);     // lower neighbour first: the chain resolves from rank 0
+        one(rank + 1, s_hi, n_hi_s, r_hi, n_hi_r, s);
+    }
+    void allreduce(double* buf, size_t n, cudaStream_t s) override {
+        stage(a, n * sizeof(double));
+        DOT_CUDA_TRY(cudaMemcpyAsync(a.data(), buf, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        DOT_CUDA_TRY(cudaStreamSynchronize(s));
+        if (t.allreduce_sum(t.ctx, reinterpret_cast<double*>(a.data()), n) != 0)
+            throw Error(DOT_ERR_CUDA, "transport allreduce failed");
+        DOT_CUDA_TRY(cudaMemcpyAsync(buf, a.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+        DOT_CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    bool synchronous() const override { return true; }
+};
+
 // DD solve of the point-combination requests: fills the field caches of every local rank.
+// Every rank runs the same multi-shift passes on its own z chunks; after each pass the two
+// boundary planes of r_{k+1} and p_k of ALL pairs are packed into one buffer per direction
+// and exchanged, and the partial sums (each rank writes only its own slots) are summed.
 void dd_solve(dot_dd* G, const std::vector<Req>& reqs) {
     const int L = (int)G->loc.size();
     dot_problem* P0 = G->loc[0];
-    const size_t N = P0->N, PS = (size_t)P0->nx * P0->ny;
+    const size_t N = P0->N;
+    const int PS = P0->nx * P0->ny;
     const int nz = P0->nz, nP = P0->nP, nf = P0->n_freq;
-    int nb = 0;
-    for (const Req& q : reqs) nb += nf * q.ncols;
-    if (nb == 0) return;
+    std::vector<Seg> segs0;
+    int n_out = 0;
+    for (const Req& q : reqs) {
+        segs0.push_back(Seg{q.side, nullptr, q.ncols});
+        n_out += nf * q.ncols;
+    }
+    if (n_out == 0) return;
+    if (nf > kMaxShift) throw Error(DOT_ERR_ARG, "more frequencies than the solver's shift capacity (8)");
+    const SeedPlan sp = plan_point(P0, segs0);
+    const int nb = sp.nseeds / 2, ns = sp.nseeds;
     const DDPlan pl = dd_plan(G, nb);
     const int ntiles = P0->tl.ntiles, nslots = ntiles * pl.C;
-    const bool use_nccl = G->comm != nullptr;
-    if (P0->tl.kind != 1) throw Error(DOT_ERR_ARG, "domain decomposition needs the z pass (DOT_COCG_KERNEL != ring)");
+    const bool local = (L == G->world);
+    std::unique_ptr<Transport> tr;
+    if (!local) {
+        if (G->comm) tr.reset(new NcclTransport(G->comm, G->rank0));
+        else tr.reset(new HostTransport(G->tr, G->rank0));
+    }
+    // sample ranges of the slabs (samples ascend by node id, slabs are contiguous node ranges)
+    std::vector<int32_t> hsamp(nP);
+    DOT_CUDA_TRY(cudaMemcpyAsync(hsamp.data(), P0->d_P.get(), nP * sizeof(int32_t), cudaMemcpyDeviceToHost, P0->stream));
+    sync(P0);
 
     struct RankBufs {
         std::vector<DBuf<double>> dcs;
-        DBuf<double2> R[2], Pv[2], XP;
-        DBuf<double> part, shift;
-        DBuf<RhsState> st;
+        DBuf<double2> R[2], Pv[2], XP, H, Ps, Xs, sbuf[2], rbuf[2];
+        DBuf<double> part;
+        DBuf<SeedState> st;
+        DBuf<ShiftState> sh;
+        DBuf<ShiftCoef> coef;
+        DBuf<uint32_t> mask;
+        DBuf<int32_t> omap;
         PassArgs a;
+        FoldArgs fa;
+        int zs = 0, ze = 0, n_lo_s = 0, n_lo_r = 0, n_hi_s = 0, n_hi_r = 0;
     };
     std::vector<RankBufs> B(L);
+    const size_t nPp = (size_t)std::max(nP, 1);
     for (int q = 0; q < L; ++q) {
         dot_problem* P = G->loc[q];
         RankBufs& b = B[q];
+        const int r = G->rank0 + q;
         std::vector<Seg> segs;
         for (const Req& rq : reqs) {
             b.dcs.emplace_back();
@@ -630,74 +798,118 @@ void dd_solve(dot_dd* G, const std::vector<Req>& reqs) {
             b.R[i] = DBuf<double2>(P->arena, (size_t)nb * N);
             b.Pv[i] = DBuf<double2>(P->arena, (size_t)nb * N);
         }
-        b.XP = DBuf<double2>(P->arena, (size_t)nb * std::max(nP, 1));
+        b.XP = DBuf<double2>(P->arena, (size_t)n_out * nPp);
+        b.H = DBuf<double2>(P->arena, (size_t)kHist * nb * nPp);
+        b.Ps = DBuf<double2>(P->arena, (size_t)ns * nf * nPp);
+        b.Xs = DBuf<double2>(P->arena, (size_t)ns * nf * nPp);
         b.part = DBuf<double>(P->arena, 2 * (size_t)nb * nslots * kNumPartials);
-        b.shift = DBuf<double>(P->arena, nb);
-        b.st = DBuf<RhsState>(P->arena, 2 * (size_t)nb);
-        build_point_rhs(P, segs, 0, nb, b.R[0].get(), b.shift.get());
-        DOT_CUDA_TRY(cudaMemsetAsync(b.XP.get(), 0, (size_t)nb * std::max(nP, 1) * sizeof(double2), P->stream));
-        DOT_CUDA_TRY(cudaMemsetAsync(b.part.get(), 0, 2 * (size_t)nb * nslots * kNumPartials * sizeof(double), P->stream));
+        b.st = DBuf<SeedState>(P->arena, 2 * (size_t)ns);
+        b.sh = DBuf<ShiftState>(P->arena, 2 * (size_t)ns * kMaxShift);
+        b.coef = DBuf<ShiftCoef>(P->arena, (size_t)kHist * ns * kMaxShift);
+        b.mask = to_device(P, sp.mask.data(), ns, DOT_HOST);
+        b.omap = to_device(P, sp.omap.data(), 3 * ns, DOT_HOST);
+        b.zs = pl.zs(r, nz);
+        b.ze = pl.ze(r, nz);
+        b.n_hi_s = r + 1 < G->world ? std::min(2, b.ze - b.zs) : 0;
+        b.n_hi_r = r + 1 < G->world ? std::min(b.ze + 2, pl.ze(r + 1, nz)) - b.ze : 0;
+        b.n_lo_s = r > 0 ? std::min(2, b.ze - b.zs) : 0;
+        b.n_lo_r = r > 0 ? std::min(2, b.zs - pl.zs(r - 1, nz)) : 0;
+        for (int d = 0; d < 2; ++d) {
+            b.sbuf[d] = DBuf<double2>(P->arena, (size_t)2 * nb * 2 * PS);
+            b.rbuf[d] = DBuf<double2>(P->arena, (size_t)2 * nb * 2 * PS);
+        }
+        cudaStream_t s = P->stream;
+        DOT_CUDA_TRY(cudaMemsetAsync(b.R[0].get(), 0, (size_t)nb * N * sizeof(double2), s));
+        DOT_CUDA_TRY(cudaMemsetAsync(b.part.get(), 0, 2 * (size_t)nb * nslots * kNumPartials * sizeof(double), s));
+        DOT_CUDA_TRY(cudaMemsetAsync(b.coef.get(), 0, (size_t)kHist * ns * kMaxShift * sizeof(ShiftCoef), s));
+        DOT_CUDA_TRY(cudaMemsetAsync(b.Ps.get(), 0, (size_t)ns * nf * nPp * sizeof(double2), s));
+        DOT_CUDA_TRY(cudaMemsetAsync(b.Xs.get(), 0, (size_t)ns * nf * nPp * sizeof(double2), s));
+        DOT_CUDA_TRY(cudaMemsetAsync(b.XP.get(), 0, (size_t)n_out * nPp * sizeof(double2), s));
+        for (int e = 0; e < ns;) {
+            const int g = sp.seg[e];
+            int e2 = e + 1;
+            while (e2 < ns && sp.seg[e2] == g && sp.col[e2] == sp.col[e2 - 1] + 1) ++e2;
+            if (g >= 0) {
+                const Seg& sg = segs[g];
+                launch_scatter_seeds(b.R[0].get(), N, sg.side == 0 ? P->d_src.get() : P->d_det.get(),
+                                     sg.side == 0 ? P->n_src : P->n_det, sg.d_coeff, sg.ncols,
+                                     sg.side == 0 ? P->d_src_scale.get() : P->d_det_scale.get(), sp.col[e], e, e2 - e,
+                                     P->op, s);
+                P->stats.kernel_launches++;
+            }
+            e = e2;
+        }
         PassArgs& a = b.a;
         a.op = P->op;
         a.tl = P->tl;
         a.max_iter = P->max_iter;
         a.tol2 = P->tol * P->tol;
+        a.nshift = nf;
+        for (int f = 0; f < nf; ++f) a.sigma[f] = P->omega[f] / P->nu;
         a.mu = P->d_mu.get();
-        a.shift = b.shift.get();
         for (int i = 0; i < 2; ++i) {
             a.R[i] = b.R[i].get();
             a.Pv[i] = b.Pv[i].get();
             a.part[i] = b.part.get() + (size_t)i * nb * nslots * kNumPartials;
-            a.st[i] = b.st.get() + (size_t)i * nb;
+            a.st[i] = b.st.get() + (size_t)i * ns;
+            a.sh[i] = b.sh.get() + (size_t)i * ns * kMaxShift;
         }
+        a.mask = b.mask.get();
+        a.coef = b.coef.get();
+        a.npairs = nb;
         a.samp_nodes = P->d_P.get();
         a.samp_off = P->d_off.get();
-        a.XP = b.XP.get();
         a.nP = nP;
-        a.X = nullptr;
-        const int r = G->rank0 + q;
+        a.H = b.H.get();
         a.zlen = pl.zlen;
         a.nzch_tot = pl.C;
         a.zc0 = pl.cb[r];
         a.nzch = pl.cb[r + 1] - pl.cb[r];
-        launch_cocg_init(a, nb, P->stream);      // full-domain sums of b: identical on every rank
-        P->stats.kernel_launches += 1;
+        FoldArgs& fa = b.fa;
+        fa.s0 = (int)(std::lower_bound(hsamp.begin(), hsamp.end(), (int32_t)((size_t)b.zs * PS)) - hsamp.begin());
+        fa.s1 = (int)(std::lower_bound(hsamp.begin(), hsamp.end(), (int32_t)((size_t)b.ze * PS)) - hsamp.begin());
+        fa.npairs = nb;
+        fa.nshift = nf;
+        fa.hist = kHist;
+        fa.nsl = nf;
+        fa.nP = (int)nPp;
+        fa.mask = b.mask.get();
+        fa.coef = b.coef.get();
+        fa.H = b.H.get();
+        fa.Ps = b.Ps.get();
+        fa.Xs = b.Xs.get();
+        launch_cg_init(a, nb, s);      // full-domain sums of b: identical on every rank
+        P->stats.kernel_launches++;
     }
-    // boundary planes [z, z + n) of vector arrays V (nb vectors of N) : (dst rank q', src rank q)
-    auto copy_planes = [&](double2* dst, const double2* src, int z, int n, cudaStream_t s) {
-        if (n <= 0) return;
-        DOT_CUDA_TRY(cudaMemcpy2DAsync(dst + (size_t)z * PS, N * sizeof(double2), src + (size_t)z * PS,
-                                       N * sizeof(double2), (size_t)n * PS * sizeof(double2), nb,
-                                       cudaMemcpyDeviceToDevice, s));
-    };
+    const size_t halo_per_plane = (size_t)2 * nb * PS;     // double2 per plane: both vectors, all pairs
     const int CHK = 8;
-    int k = 0;
+    int k = 0, g = 0, kf = 0;
     for (;;) {
         const int kout = (k + 1) & 1;
         for (int q = 0; q < L; ++q) {
             dot_problem* P = G->loc[q];
             PassArgs& a = B[q].a;
             a.k = k;
-            if (use_nccl)   // this rank's slots only; the others arrive through the all-reduce
+            if (!local)   // this rank's slots only; the others arrive through the sum
                 DOT_CUDA_TRY(cudaMemsetAsync(a.part[kout], 0, (size_t)nb * nslots * kNumPartials * sizeof(double),
                                              P->stream));
-            launch_cocg_pass(a, nb, P->stream);
+            launch_cg_pass(a, nb, P->stream);
             P->stats.kernel_launches++;
             P->stats.pass_launches++;
+            RankBufs& b = B[q];
+            // pack the boundary planes of r_{k+1}, p_k (kout arrays) for the neighbours
+            launch_pack_planes(a.R[kout], a.Pv[kout], nb, N, PS, b.zs, b.n_lo_s, b.sbuf[0].get(), P->stream);
+            launch_pack_planes(a.R[kout], a.Pv[kout], nb, N, PS, b.ze - b.n_hi_s, b.n_hi_s, b.sbuf[1].get(), P->stream);
+            P->stats.kernel_launches += 2;
         }
-        // ---- halo exchange of r_{k+1}, p_k (kout arrays) and all-reduce of the partials
-        if (!use_nccl) {
+        if (local) {
             for (int q = 0; q < L; ++q) DOT_CUDA_TRY(cudaStreamSynchronize(G->loc[q]->stream));
             cudaStream_t s = G->loc[0]->stream;
             for (int q = 0; q + 1 < L; ++q) {
-                const int r = G->rank0 + q;
-                const int zt = pl.ze(r, nz);                         // boundary between r and r + 1
-                for (int v = 0; v < 2; ++v) {
-                    double2* lo = v == 0 ? B[q].a.R[kout] : B[q].a.Pv[kout];
-                    double2* hi = v == 0 ? B[q + 1].a.R[kout] : B[q + 1].a.Pv[kout];
-                    copy_planes(hi, lo, std::max(zt - 2, pl.zs(r, nz)), std::min(2, zt - pl.zs(r, nz)), s);
-                    copy_planes(lo, hi, zt, std::min(zt + 2, pl.ze(r + 1, nz)) - zt, s);
-                }
+                DOT_CUDA_TRY(cudaMemcpyAsync(B[q + 1].rbuf[0].get(), B[q].sbuf[1].get(),
+                                             B[q + 1].n_lo_r * halo_per_plane * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+                DOT_CUDA_TRY(cudaMemcpyAsync(B[q].rbuf[1].get(), B[q + 1].sbuf[0].get(),
+                                             B[q].n_hi_r * halo_per_plane * sizeof(double2), cudaMemcpyDeviceToDevice, s));
             }
             for (int q = 0; q < L; ++q)            // owned slot ranges to every other local rank
                 for (int q2 = 0; q2 < L; ++q2) {
@@ -706,89 +918,104 @@ void dd_solve(dot_dd* G, const std::vector<Req>& reqs) {
                     const size_t off = (size_t)pl.cb[r] * ntiles * kNumPartials;
                     const size_t w = (size_t)(pl.cb[r + 1] - pl.cb[r]) * ntiles * kNumPartials * sizeof(double);
                     DOT_CUDA_TRY(cudaMemcpy2DAsync(B[q2].a.part[kout] + off, nslots * kNumPartials * sizeof(double),
-                                                   B[q].a.part[kout] + off, nslots * kNumPartials * sizeof(double),
-                                                   w, nb, cudaMemcpyDeviceToDevice, s));
+                                                   B[q].a.part[kout] + off, nslots * kNumPartials * sizeof(double), w,
+                                                   nb, cudaMemcpyDeviceToDevice, s));
                 }
             DOT_CUDA_TRY(cudaStreamSynchronize(s));
         } else {
-            NcclApi& nc = nccl_api();
-            dot_problem* P = G->loc[0];
-            const int r = G->rank0;
-            const int zs = pl.zs(r, nz), ze = pl.ze(r, nz);
-            DOT_NCCL_TRY(nc.groupStart());
-            for (int v = 0; v < 2; ++v) {
-                double2* X = v == 0 ? B[0].a.R[kout] : B[0].a.Pv[kout];
-                for (int i = 0; i < nb; ++i) {
-                    double2* Xi = X + (size_t)i * N;
-                    if (r + 1 < G->world) {                 // top planes up, halo from above
-                        const int n_up = std::min(2, ze - zs), n_dn = std::min(ze + 2, pl.ze(r + 1, nz)) - ze;
-                        DOT_NCCL_TRY(nc.send(Xi + (size_t)(ze - n_up) * PS, 2 * n_up * PS, ncclDouble, r + 1, G->comm,
-                                             P->stream));
-                        DOT_NCCL_TRY(nc.recv(Xi + (size_t)ze * PS, 2 * n_dn * PS, ncclDouble, r + 1, G->comm, P->stream));
-                    }
-                    if (r > 0) {                            // bottom planes down, halo from below
-                        const int n_dn = std::min(2, ze - zs), n_up = std::min(2, zs - pl.zs(r - 1, nz));
-                        DOT_NCCL_TRY(nc.send(Xi + (size_t)zs * PS, 2 * n_dn * PS, ncclDouble, r - 1, G->comm, P->stream));
-                        DOT_NCCL_TRY(nc.recv(Xi + (size_t)(zs - n_up) * PS, 2 * n_up * PS, ncclDouble, r - 1, G->comm,
-                                             P->stream));
-                    }
-                }
-            }
-            DOT_NCCL_TRY(nc.groupEnd());
-            DOT_NCCL_TRY(nc.allReduce(B[0].a.part[kout], B[0].a.part[kout], (size_t)nb * nslots * kNumPartials,
-                                      ncclDouble, ncclSum, G->comm, P->stream));
+            RankBufs& b = B[0];
+            cudaStream_t s = G->loc[0]->stream;
+            tr->halo(b.sbuf[0].get(), b.n_lo_s * halo_per_plane, b.rbuf[0].get(), b.n_lo_r * halo_per_plane,
+                     b.sbuf[1].get(), b.n_hi_s * halo_per_plane, b.rbuf[1].get(), b.n_hi_r * halo_per_plane, s);
+            tr->allreduce(b.a.part[kout], (size_t)nb * nslots * kNumPartials, s);
+        }
+        for (int q = 0; q < L; ++q) {
+            dot_problem* P = G->loc[q];
+            RankBufs& b = B[q];
+            PassArgs& a = b.a;
+            launch_unpack_planes(a.R[kout], a.Pv[kout], nb, N, PS, b.zs - b.n_lo_r, b.n_lo_r, b.rbuf[0].get(), P->stream);
+            launch_unpack_planes(a.R[kout], a.Pv[kout], nb, N, PS, b.ze, b.n_hi_r, b.rbuf[1].get(), P->stream);
+            P->stats.kernel_launches += 2;
         }
         ++k;
-        if (k % CHK == 0 || k > P0->max_iter) {
+        if (k - kf >= kHist) {
+            for (int q = 0; q < L; ++q) {
+                B[q].fa.k0 = kf;
+                B[q].fa.k1 = k;
+                launch_cg_fold(B[q].fa, G->loc[q]->stream);
+                G->loc[q]->stats.kernel_launches++;
+            }
+            kf = k;
+        }
+        if (k % CHK == 0) {   // pipelined poll (every rank holds the same scalars; rank 0's count)
             dot_problem* P = G->loc[0];
-            launch_count_active(B[0].a.st[(k - 1) & 1], nb, P->d_count.get(), P->stream);
-            DOT_CUDA_TRY(cudaMemcpyAsync(P->h_count, P->d_count.get(), sizeof(int), cudaMemcpyDeviceToHost, P->stream));
-            sync(P);
-            if (*P->h_count == 0) break;
+            launch_count_active(B[0].a.st[(k - 1) & 1], nb, P->d_count.get() + (g & 1), P->stream);
+            DOT_CUDA_TRY(cudaMemcpyAsync(P->h_count + (g & 1), P->d_count.get() + (g & 1), sizeof(int),
+                                         cudaMemcpyDeviceToHost, P->stream));
+            DOT_CUDA_TRY(cudaEventRecord(P->poll_ev[g & 1], P->stream));
+            bool stop = false;
+            if (local || (tr && tr->synchronous())) {
+                DOT_CUDA_TRY(cudaEventSynchronize(P->poll_ev[g & 1]));
+                stop = P->h_count[g & 1] == 0;
+            } else if (g > 0) {
+                DOT_CUDA_TRY(cudaEventSynchronize(P->poll_ev[(g - 1) & 1]));
+                stop = P->h_count[(g - 1) & 1] == 0;
+            }
+            ++g;
+            if (stop) break;
         }
     }
-    // ---- sampled solutions: each sample node belongs to one slab -> sum over ranks
-    const size_t nx = (size_t)nb * std::max(nP, 1);
-    if (!use_nccl) {
-        for (int q = 1; q < L; ++q) launch_cadd_inplace(B[0].XP.get(), B[q].XP.get(), nx, G->loc[0]->stream);
+    // ---- shifted solutions on each rank's own samples, then the sum over ranks
+    const size_t nx = (size_t)n_out * nPp;
+    for (int q = 0; q < L; ++q) {
+        dot_problem* P = G->loc[q];
+        B[q].fa.k0 = kf;
+        B[q].fa.k1 = k;
+        launch_cg_fold(B[q].fa, P->stream);
+        launch_cg_finalize(B[q].fa, P->op, B[q].XP.get(), nP, B[q].omap.get(), P->d_P.get(), P->stream);
+        P->stats.kernel_launches += 2;
+    }
+    if (local) {
+        for (int q = 0; q < L; ++q) DOT_CUDA_TRY(cudaStreamSynchronize(G->loc[q]->stream));
+        cudaStream_t s = G->loc[0]->stream;
+        for (int q = 1; q < L; ++q) launch_cadd_inplace(B[0].XP.get(), B[q].XP.get(), nx, s);
         for (int q = 1; q < L; ++q)
-            DOT_CUDA_TRY(cudaMemcpyAsync(B[q].XP.get(), B[0].XP.get(), nx * sizeof(double2), cudaMemcpyDeviceToDevice,
-                                         G->loc[0]->stream));
-        DOT_CUDA_TRY(cudaStreamSynchronize(G->loc[0]->stream));
+            DOT_CUDA_TRY(cudaMemcpyAsync(B[q].XP.get(), B[0].XP.get(), nx * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+        DOT_CUDA_TRY(cudaStreamSynchronize(s));
     } else {
-        DOT_NCCL_TRY(nccl_api().allReduce(B[0].XP.get(), B[0].XP.get(), 2 * nx, ncclDouble, ncclSum, G->comm,
-                                          G->loc[0]->stream));
+        tr->allreduce(reinterpret_cast<double*>(B[0].XP.get()), 2 * nx, G->loc[0]->stream);
     }
     // ---- convergence flags, statistics and the field caches of every local rank
     for (int q = 0; q < L; ++q) {
         dot_problem* P = G->loc[q];
-        std::vector<RhsState> hs(nb);
-        DOT_CUDA_TRY(cudaMemcpyAsync(hs.data(), B[q].a.st[(k - 1) & 1], nb * sizeof(RhsState), cudaMemcpyDeviceToHost,
+        std::vector<SeedState> hs(ns);
+        DOT_CUDA_TRY(cudaMemcpyAsync(hs.data(), B[q].a.st[(k - 1) & 1], ns * sizeof(SeedState), cudaMemcpyDeviceToHost,
                                      P->stream));
         sync(P);
         int mx = 0, mn = 1 << 30;
-        for (int i = 0; i < nb; ++i) {
-            if (hs[i].flag == DOT_ERR_NOCONV) throw Error(DOT_ERR_NOCONV, "COCG (domain decomposition) did not converge");
-            if (hs[i].flag == DOT_ERR_BREAKDOWN) throw Error(DOT_ERR_BREAKDOWN, "COCG (domain decomposition) breakdown");
-            mx = std::max(mx, hs[i].iters);
-            mn = std::min(mn, hs[i].iters);
-            P->stats.rhs_iterations += hs[i].iters;
-            P->stats.pass_bytes += 64.0 * (double)N * hs[i].iters / G->world;
+        for (int i = 0; i < ns; ++i) {
+            if (!sp.mask[i]) continue;
+            if (hs[i].flag == DOT_ERR_NOCONV) throw Error(DOT_ERR_NOCONV, "CG (domain decomposition) did not converge");
+            if (hs[i].flag == DOT_ERR_BREAKDOWN) throw Error(DOT_ERR_BREAKDOWN, "CG (domain decomposition) breakdown");
+            const int it = hs[i].iters, systems = __builtin_popcount(sp.mask[i]);
+            mx = std::max(mx, it);
+            mn = std::min(mn, it);
+            P->stats.seeds_solved++;
+            P->stats.seed_iterations += it;
+            P->stats.rhs_solved += systems;
+            P->stats.rhs_iterations += (int64_t)systems * it;
+            P->stats.pass_bytes += 32.0 * (double)N * it / G->world;
         }
-        P->stats.rhs_solved += nb;
         P->stats.last_max_iters = mx;
         P->stats.last_min_iters = mn;
         size_t off = 0;
-        const size_t nPp = (size_t)std::max(nP, 1);
+        auto blk = std::make_shared<DBuf<double2>>(std::move(B[q].XP));
         for (const Req& rq : reqs) {
             const int n_side = rq.side == 0 ? P->n_src : P->n_det;
             FieldCache& c = P->cache[rq.side];
-            c.valid = false;
-            c.X.reset();
             const size_t n = (size_t)nf * rq.ncols * nPp;
-            c.X = DBuf<double2>(P->arena, n);
-            DOT_CUDA_TRY(cudaMemcpyAsync(c.X.get(), B[q].XP.get() + off, n * sizeof(double2), cudaMemcpyDeviceToDevice,
-                                         P->stream));
+            c.blk = blk;
+            c.X = blk->get() + off;
             off += n;
             c.valid = true;
             c.identity = rq.identity;
@@ -863,22 +1090,12 @@ int dot_create(const dot_config* cfg, dot_problem** out) {
         P->op.robin = 1.0 / (2.0 * P->hz);
         P->op.dint = 2.0 * P->op.cx + 2.0 * P->op.cy + 2.0 * P->op.cz;
         {
-            // tuning knobs: planes prefetched, smem budget per CTA
-            const char* ePD = std::getenv("DOT_COCG_PREFETCH");
-            const char* eSM = std::getenv("DOT_COCG_SMEM_KB");
-            const char* eTH = std::getenv("DOT_COCG_THREADS");
-            const char* eK = std::getenv("DOT_COCG_KERNEL");      // "ring" selects the padded-ring pass
-            const char* eTY = std::getenv("DOT_COCG_TY");         // z-pass tile height
-            const int kind = (eK && std::string(eK) == "ring") ? 0 : 1;
-            const int pd = ePD ? std::max(1, std::atoi(ePD)) : (kind == 1 ? 2 : 1);
-            const size_t sm = eSM ? (size_t)std::atoi(eSM) * 1024 : 0;
-            P->tl = cocg_tiling(P->nx, P->ny, P->nz, pd, sm, eTH ? std::atoi(eTH) : 0, kind,
-                                eTY ? std::atoi(eTY) : 0);
-            // cluster of consecutive tiles of one RHS: the largest size <= request dividing ntiles
-            const char* eCL = std::getenv("DOT_COCG_CLUSTER");
-            int cs = eCL ? std::max(1, std::min(8, std::atoi(eCL))) : 1;
-            while (cs > 1 && P->tl.ntiles % cs != 0) --cs;
-            P->tl.cluster = cs;
+            // test knobs: TMA planes in flight, forced tile height
+            const char* ePD = std::getenv("DOT_CG_PREFETCH");
+            const char* eTY = std::getenv("DOT_CG_TY");
+            const char* eRW = std::getenv("DOT_CG_ROWS");
+            P->tl = cg_tiling(P->nx, P->ny, P->nz, ePD ? std::max(1, std::atoi(ePD)) : 2, eTY ? std::atoi(eTY) : 0,
+                              eRW ? std::atoi(eRW) : 0);
         }
         P->pc = PalsConst{P->nx, P->ny, P->nz, P->n_rbf, P->hx, P->hy, P->hz, P->gamma, P->eps, P->cutoff,
                           P->mua_in, P->mua_out};
@@ -915,13 +1132,19 @@ size_t dot_workspace_bytes(const dot_problem* P, int32_t max_rhs) {
     if (!P) return 0;
     const size_t N = P->N;
     size_t fixed = N * (sizeof(double) + 4 * sizeof(int32_t)) + scan_temp_bytes(N) + 64 * 1024;
-    // support / samples: budget 5% of the nodes
-    const size_t Kb = N / 20 + P->n_det;
+    // support / samples: budget 5% of the nodes on large grids, every node on small ones
+    const size_t Kb = std::min(N, std::max(N / 20 + P->n_det + P->n_src, (size_t)65536));
     fixed += Kb * (3 * sizeof(int32_t) + P->n_p * sizeof(double)) + (size_t)P->nz * P->tl.ntiles * 4;
     fixed += (size_t)P->n_freq * P->n_src * P->n_det * sizeof(double2);
-    // field caches (sources + detectors, all frequencies) on the samples
-    fixed += (size_t)P->n_freq * (P->n_src + P->n_det) * Kb * sizeof(double2);
-    return fixed + (size_t)std::max(max_rhs, 1) * per_rhs_bytes(P) + 64 * Arena::kAlign;
+    // field caches (sources + detectors, all frequencies) on the samples, plus as much again for
+    // the Jacobian's support panels / combined fields, and the host-staged full Jacobian
+    fixed += 2 * (size_t)P->n_freq * (P->n_src + P->n_det) * Kb * sizeof(double2);
+    fixed += (size_t)P->n_freq * P->n_src * P->n_det * std::max(P->n_p, 1) * sizeof(double2);
+    // max_rhs systems = max_rhs / n_freq real seeds (all shifts of one seed together), in pairs
+    const size_t pairs = ((size_t)std::max(max_rhs, 1) + 2 * P->n_freq - 1) / (2 * P->n_freq) + 1;
+    // dense solutions (dot_solve: every node sampled) of up to 3 complex right-hand sides
+    const size_t dense = 3 * per_pair_bytes(P, (int)N, 8, 1) + 6 * N * sizeof(double2);
+    return fixed + std::max(pairs * per_pair_bytes(P, (int)Kb, kHist, P->n_freq), dense) + 64 * Arena::kAlign;
 }
 
 int dot_bind_workspace(dot_problem* P, void* ptr, size_t bytes) {
@@ -1205,7 +1428,8 @@ int dot_optimize_directions_subspace(dot_problem* P, int32_t k, int32_t iters, i
     ops.fields = [&](int side, const std::vector<double>& coeff, int ncols, double2* out) {
         DBuf<double> dc = to_device(P, coeff.data(), coeff.size(), DOT_HOST);
         DBuf<double2> XP(P->arena, std::max<size_t>((size_t)nf * ncols * nP, 1));
-        solve_rhs(P, side, dc.get(), ncols, nf * ncols, nullptr, nullptr, XP.get(), nullptr);
+        solve_batch(P, {Seg{side, dc.get(), ncols}}, nullptr, {}, XP.get(), nf * ncols, nP, P->d_P.get(),
+                    P->d_off.get());
         launch_gather_cols(nf, ncols, K, XP.get(), (size_t)ncols * nP, nP, P->d_S_slot.get(), out, (size_t)ncols * K,
                            K, s);
         P->stats.kernel_launches++;
@@ -1218,9 +1442,8 @@ int dot_optimize_directions_subspace(dot_problem* P, int32_t k, int32_t iters, i
         launch_scatter_support(R.get(), P->N, nr, P->d_S.get(), K, w, s);
         std::vector<int32_t> fo(nr);
         for (int r = 0; r < nr; ++r) fo[r] = r / nvec;
-        DBuf<int32_t> dfo = to_device(P, fo.data(), fo.size(), DOT_HOST);
         DBuf<double2> XP(P->arena, std::max<size_t>((size_t)nr * nP, 1));
-        solve_rhs(P, -1, nullptr, 1, nr, R.get(), dfo.get(), XP.get(), nullptr);
+        solve_batch(P, {}, R.get(), fo, XP.get(), nr, nP, P->d_P.get(), P->d_off.get());
         const int n_side = side == 0 ? P->n_src : P->n_det;
         launch_gather_cols(nf, nvec, n_side, XP.get(), (size_t)nvec * nP, nP,
                            side == 0 ? P->d_src_slot.get() : P->d_det_slot.get(), out, (size_t)nvec * n_side, n_side, s);
@@ -1339,9 +1562,21 @@ int dot_solve(dot_problem* P, int32_t nrhs, const int32_t* freq, const double* b
     require_params(P);
     const size_t n = (size_t)nrhs * P->N;
     DBuf<double2> db = to_device(P, reinterpret_cast<const double2*>(b), n, where);
-    DBuf<int32_t> df = to_device(P, freq, nrhs, where);
+    std::vector<int32_t> fh(nrhs);
+    if (where == DOT_HOST) {
+        std::copy(freq, freq + nrhs, fh.begin());
+    } else {
+        DOT_CUDA_TRY(cudaMemcpyAsync(fh.data(), freq, nrhs * sizeof(int32_t), cudaMemcpyDeviceToHost, P->stream));
+        sync(P);
+    }
+    // dense solutions: the sample list is every node (identity), with its (plane, tile) ranges
+    std::vector<int32_t> all(P->N);
+    for (size_t i = 0; i < P->N; ++i) all[i] = (int32_t)i;
+    DBuf<int32_t> dall = to_device(P, all.data(), all.size(), DOT_HOST);
+    DBuf<int32_t> doff(P->arena, (size_t)P->nz * P->tl.ntiles + 1);
+    launch_sample_offsets(dall.get(), (int)P->N, P->nx, P->ny, P->nz, P->tl.TY, P->tl.ntiles, doff.get(), P->stream);
     DBuf<double2> dx(P->arena, n);
-    auto it = solve_rhs(P, -1, nullptr, 1, nrhs, db.get(), df.get(), nullptr, dx.get());
+    auto it = solve_batch(P, {}, db.get(), fh, dx.get(), nrhs, (int)P->N, dall.get(), doff.get());
     from_device(P, reinterpret_cast<double2*>(x), dx.get(), n, where);
     sync(P);
     if (iters_out) std::copy(it.begin(), it.end(), iters_out);
@@ -1440,6 +1675,24 @@ int dot_dd_create(dot_problem* const* local, int32_t nlocal, int32_t rank0, int3
     }
 }
 
+int dot_dd_create_transport(dot_problem* local, int32_t rank, int32_t world, const dot_transport* t, dot_dd** out) {
+    try {
+        if (!local || !out || !t || !t->sendrecv || !t->allreduce_sum || world < 2 || rank < 0 || rank >= world)
+            throw Error(DOT_ERR_ARG, "bad transport decomposition arguments");
+        std::unique_ptr<dot_dd> G(new dot_dd());
+        G->loc.push_back(local);
+        G->rank0 = rank;
+        G->world = world;
+        G->host = true;
+        G->tr = *t;
+        *out = G.release();
+        return DOT_OK;
+    } catch (const Error& e) {
+        g_create_error = e.msg;
+        return e.code;
+    }
+}
+
 int dot_dd_destroy(dot_dd* G) {
     if (!G) return DOT_OK;
     if (G->comm) nccl_api().commDestroy(G->comm);
@@ -1468,7 +1721,8 @@ int dot_dd_fields(dot_dd* G, const double* W, int32_t ls, const double* V, int32
         for (dot_problem* Q : G->loc)
             for (auto& c : Q->cache) {
                 c.valid = false;
-                c.X.reset();
+                c.blk.reset();
+                c.X = nullptr;
             }
         dd_solve(G, reqs);
         return DOT_OK;

@@ -87,17 +87,30 @@ __device__ __forceinline__ double2 diag_of(const OpConst& c, int k, double mu, d
     return make_double2(th * (2.0 * c.cx + 2.0 * c.cy + mu) + c.cz * nzn + rob, th * shift);
 }
 
-// Per-RHS COCG scalar state (double buffered by pass parity).
-struct RhsState {
-    double rho_re, rho_im;     // rho_k = r_k^T r_k (bilinear)
-    double alpha_re, alpha_im; // alpha_k
-    double bnorm2;             // ||b||_2^2
+// Multi-shift CG state (cg_shift.cu).
+constexpr int kMaxShift = 8;       // frequencies solved by one real seed
+constexpr int kHist = 16;          // passes between folds of the shifted recurrences (history ring)
+constexpr int kNumPartials = 8;    // per pair of seeds: rho(2) mu(2) nu(2) sigma_direct(2)
+
+// Per-seed real CG state (double buffered by pass parity).
+struct SeedState {
+    double rho;                // rho_k = r_k^T r_k
+    double alpha;              // alpha_k of the last active pass (a_{k-1} for the next one)
+    double bnorm2;             // ||b~||_2^2
     int32_t done;              // 1 once converged / failed
     int32_t iters;             // iterations at convergence
     int32_t flag;              // 0 ok, DOT_ERR_NOCONV, DOT_ERR_BREAKDOWN
     int32_t pad;
 };
-
-constexpr int kNumPartials = 9;   // rho(2) mu(2) nu(2) sigma_direct(2) |r|^2
+// Per (seed, shift): zeta_{k-1}, zeta_k of the shifted residuals r_sigma = zeta r.
+struct ShiftState {
+    double2 zp, zc;
+};
+// Fold record of pass k for one (seed, shift): p_s <- zeta r_k + beta p_s; x_s += alpha p_s.
+struct ShiftCoef {
+    double2 zeta, beta, alpha;
+    int32_t k;                 // pass the record belongs to (stale records are skipped)
+    int32_t active;
+};
 
 }  // namespace dot

@@ -5,89 +5,86 @@
 
 namespace dot {
 
-// ------------------------------------------------------------------ cocg.cu
-// Tiling of the fused COCG pass: a CTA owns TY full x-rows of one RHS and
-// marches all nz planes; planes (with a 2-row y halo) are staged by TMA bulk
+// ------------------------------------------------------------------ cg_shift.cu
+// Tiling of the fused multi-shift CG pass: a CTA owns TY full x-rows of one pair of real
+// seeds and marches the nz planes; planes (with a 2-row y halo) are staged by TMA bulk
 // copies into a ring of `nslots` shared-memory slots.
-struct CocgTiling {
-    int kind = 1;         // 1: z-register pass (cocg_z.cu), 0: padded-ring pass (cocg.cu)
-    int cluster = 1;      // thread-block cluster size along the tiles of one RHS (divides ntiles)
-    int minb = 1;         // CTAs per SM the z pass is compiled for
-    int zrows = 1;        // z pass: slot rows per thread (1 or 2)
+struct CgTiling {
+    int rows = 2;         // slot rows per thread (1 or 2)
     int TY = 0, ntiles = 0, nslots = 0, threads = 512;
-    int rpt = 0;          // x-rows covered by one sweep of the block (threads = roundup32(nx * rpt))
     size_t smem = 0;
 };
-// prefetch: planes loaded ahead (slots = prefetch + 3); max_smem: per-CTA budget (bytes)
-// kind: 1 = z-register pass if a tiling fits (else the ring pass), 0 = ring pass;
-// want_ty > 0 forces the z-pass tile height.
-CocgTiling cocg_tiling(int nx, int ny, int nz, int prefetch = 1, size_t max_smem = 0, int max_threads = 0,
-                       int kind = 1, int want_ty = 0);
+// prefetch: planes loaded ahead (1..3; slots = prefetch + 2); want_ty > 0 forces the tile height,
+// want_rows > 0 the rows per thread
+CgTiling cg_tiling(int nx, int ny, int nz, int prefetch = 2, int want_ty = 0, int want_rows = 0);
+size_t pass_smem(int nx, int TY, int NS, int nz);
 
 struct PassArgs {
     OpConst op;
-    CocgTiling tl;
+    CgTiling tl;
     int k = 0;                    // pass index
-    int nzch = 1;                 // z chunks launched per (tile, RHS) (z pass only)
+    int nzch = 1;                 // z chunks launched per (tile, pair)
     int zlen = 0;                 // planes per z chunk
     int zc0 = 0;                  // first (global) z chunk of this launch (z-slab domain decomposition)
-    int nzch_tot = 1;             // global z chunks: partial slots per RHS = ntiles * nzch_tot
-    const int32_t* act = nullptr; // z pass: grid row y iterates RHS act[y] (active list), null = identity
+    int nzch_tot = 1;             // global z chunks: partial slots per pair = ntiles * nzch_tot
+    const int32_t* act = nullptr; // grid row y iterates pair act[y] (active list), null = identity
     int max_iter = 0;
     double tol2 = 0;              // tol^2
+    int nshift = 0;               // frequencies (shifts i omega_f / nu of the scaled system)
+    double sigma[kMaxShift] = {}; // omega_f / nu
     const double* mu = nullptr;   // [N] absorption
-    const double* shift = nullptr;// [nb] omega/nu of each RHS
-    double2* R[2] = {nullptr, nullptr};   // [nb][N] residual r (ping-pong)
-    double2* Pv[2] = {nullptr, nullptr};  // [nb][N] direction p (ping-pong)
-    double* part[2] = {nullptr, nullptr}; // [nb][ntiles][kNumPartials]
-    RhsState* st[2] = {nullptr, nullptr}; // [nb]
+    double2* R[2] = {nullptr, nullptr};   // [npairs][N] residual r~ of two real seeds (ping-pong)
+    double2* Pv[2] = {nullptr, nullptr};  // [npairs][N] direction p~ (ping-pong)
+    double* part[2] = {nullptr, nullptr}; // [npairs][nzch_tot][ntiles][kNumPartials]
+    SeedState* st[2] = {nullptr, nullptr};// [2 npairs]
+    ShiftState* sh[2] = {nullptr, nullptr};// [2 npairs][kMaxShift]
+    const uint32_t* mask = nullptr;       // [2 npairs] shifts each seed must deliver
+    ShiftCoef* coef = nullptr;            // [hist][2 npairs][kMaxShift]
+    int hist = kHist;                     // depth of the coef / H rings (passes between folds)
+    int npairs = 0;                       // pairs of the batch (strides of coef / H)
     const int32_t* samp_nodes = nullptr;  // [nP] ascending node ids
     const int32_t* samp_off = nullptr;    // [nz*ntiles+1] ranges of samples per (plane, tile)
-    double2* XP = nullptr;                // [nb][nP] sampled solution
     int nP = 0;
-    double2* X = nullptr;                 // [nb][N] full solution (test mode) or null
+    double2* H = nullptr;                 // [hist][npairs][nP] seed residual r_k at the samples
 };
 
-// Launch a pass kernel, as a thread-block cluster of `cs` consecutive tiles of one
-// RHS when cs > 1 (co-scheduled, so y-halo rows read by neighbours hit in L2).
-template <class K>
-void launch_clustered(K kernel, dim3 grid, int threads, size_t smem, cudaStream_t s, int cs, const PassArgs& a) {
-    if (cs <= 1) {
-        kernel<<<grid, threads, smem, s>>>(a);
-    } else {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = grid;
-        cfg.blockDim = dim3(threads);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = cs;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        DOT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, a));
-    }
-    DOT_CUDA_TRY(cudaGetLastError());
-}
+struct FoldArgs {
+    int k0 = 0, k1 = 0;                   // passes to fold
+    int s0 = 0, s1 = 0;                   // sample range
+    int npairs = 0, nshift = 0, nP = 0;
+    int hist = kHist;                     // ring depth
+    int nsl = 0;                          // shift slots per seed (needed shifts in ascending order)
+    const uint32_t* mask = nullptr;
+    const ShiftCoef* coef = nullptr;
+    const double2* H = nullptr;
+    double2* Ps = nullptr;                // [2 npairs][nsl][nP] shifted directions on the samples
+    double2* Xs = nullptr;                // [2 npairs][nsl][nP] shifted solutions (scaled variables)
+};
 
-// z-register pass (cocg_z.cu)
-size_t zpass_smem(int nx, int TY, int NS, int nz);
-void launch_cocg_zpass(const PassArgs& a, int nb, cudaStream_t s);
-void launch_cocg_init(const PassArgs& a, int nb, cudaStream_t s);
-void launch_cocg_pass(const PassArgs& a, int nb, cudaStream_t s);
-// *d_count = number of RHS not done; act (optional, [nb]) receives their indices in order
-void launch_count_active(const RhsState* st, int nb, int* d_count, cudaStream_t s, int32_t* act = nullptr);
+void launch_cg_pass(const PassArgs& a, int nb, cudaStream_t s);
+// zc_own: the z-chunk slot that carries the initial sums (0)
+void launch_cg_init(const PassArgs& a, int nb, cudaStream_t s, int zc_own = 0);
+void launch_cg_fold(const FoldArgs& f, cudaStream_t s);
+// omap[3 seed] = (output base, output stride per shift, 1 if the seed is the imaginary part)
+void launch_cg_finalize(const FoldArgs& f, const OpConst& op, double2* XP, int nP_out, const int32_t* omap,
+                        const int32_t* samp_nodes, cudaStream_t s);
+// *d_count = number of pairs with a seed not done; act (optional, [npairs]) receives them in order
+void launch_count_active(const SeedState* st, int npairs, int* d_count, cudaStream_t s, int32_t* act = nullptr);
+// A(omega, p) u in the original variables (dot_apply)
 void launch_apply(const OpConst& op, const double* mu, const double* shift, const double2* u,
                   double2* Au, int nb, cudaStream_t s);
-// Chunk of the global RHS list r = f*ncols + c (r = rg0 .. rg0+nb-1):
-// R0[r][node[a]] = coeff[a*ncols + c] * scale[a]  (coeff == null: identity)
-void launch_scatter_rhs(double2* R0, size_t N, int nb, long long rg0, int ncols, const int32_t* nodes,
-                        int nnodes, const double* coeff, const double* scale, cudaStream_t s);
-// shift[r] = omega_over_nu[(rg0 + r) / ncols]
-void launch_fill_shift(double* shift, int nb, long long rg0, int ncols, const double* omega_over_nu,
-                       cudaStream_t s);
+// chunk-local seeds seed0 .. seed0+nseeds-1 (pair = seed / 2, component = seed % 2) are the
+// columns col0 .. of one segment: R0[pair][node[a]] = coeff[a*ncols + col] * scale[a] * theta^-1/2
+// (coeff null: identity)
+void launch_scatter_seeds(double2* R0, size_t N, const int32_t* nodes, int nnodes, const double* coeff, int ncols,
+                          const double* scale, int col0, int seed0, int nseeds, const OpConst& op, cudaStream_t s);
+// z-slab halo planes z0 .. z0+n-1 of r and p of every pair <-> buf [2][npairs][n][PS]
+void launch_pack_planes(const double2* R, const double2* Pv, int npairs, size_t N, int PS, int z0, int n,
+                        double2* buf, cudaStream_t s);
+void launch_unpack_planes(double2* R, double2* Pv, int npairs, size_t N, int PS, int z0, int n, const double2* buf,
+                          cudaStream_t s);
+// dense complex RHS r -> pair r = (Re, Im) * theta^-1/2
+void launch_split_dense(double2* R0, const double2* b, size_t N, int nr, const OpConst& op, cudaStream_t s);
 
 // ------------------------------------------------------------------ pals.cu
 struct PalsConst {

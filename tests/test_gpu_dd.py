@@ -91,7 +91,7 @@ def test_dd_rejects_too_many_ranks(dot):
     cfg = small_config(n=(8, 8, 5), eps=0.4)
     prob, wl = small_problem(cfg, with_data=False)
     ranks = []
-    for _ in range(3):
+    for _ in range(4):                 # nz = 5: 3 slabs of >= 2 planes at most
         g = dot.DOTProblem.from_config(cfg, wl.src_nodes, wl.det_nodes)
         g.set_params(wl.p)
         ranks.append(g)

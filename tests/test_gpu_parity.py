@@ -283,10 +283,10 @@ def test_optimize_directions_subspace_converges_to_exact(dot):
     assert abs(float(Ws[:, -1] @ We[:, -1])) / 12 > 1 - 1e-8
 
 
-@pytest.mark.parametrize("knobs", [dict(DOT_COCG_ZCHUNKS="1"), dict(DOT_COCG_ZCHUNKS="2"),
-                                   dict(DOT_COCG_ZCHUNKS="3"), dict(DOT_COCG_ZCHUNKS="4"),
-                                   dict(DOT_COCG_ZCHUNKS="3", DOT_COCG_ZOPT="B"),
-                                   dict(DOT_COCG_ZCHUNKS="4", DOT_COCG_ZOPT="D", DOT_COCG_TY="5")])
+@pytest.mark.parametrize("knobs", [dict(DOT_CG_ZCHUNKS="1"), dict(DOT_CG_ZCHUNKS="2"),
+                                   dict(DOT_CG_ZCHUNKS="3"), dict(DOT_CG_ZCHUNKS="4"),
+                                   dict(DOT_CG_ZCHUNKS="3", DOT_CG_ROWS="1"),
+                                   dict(DOT_CG_ZCHUNKS="4", DOT_CG_ROWS="2", DOT_CG_TY="5")])
 def test_z_chunks_keep_parity(dot, knobs, monkeypatch):
     """z-chunked passes (each chunk recomputes 2 halo planes of p and 1 of r_{k+1},
     DESIGN.md "z chunks") solve the same systems: nz = 19 splits into 10+9, 7+7+5, 5+5+5+4."""
@@ -310,16 +310,10 @@ def test_z_chunks_keep_parity(dot, knobs, monkeypatch):
     assert rel(J, jacobian(prob, wl.p, np.eye(cfg.n_s), np.eye(cfg.n_d))) < 1e-7
 
 
-RING = dict(DOT_COCG_KERNEL="ring")
-KNOBS = [dict(RING, DOT_COCG_THREADS="256"), dict(RING, DOT_COCG_THREADS="128"),
-         dict(RING, DOT_COCG_SMEM_KB="64"), dict(RING, DOT_COCG_PREFETCH="2"),
-         dict(RING, DOT_COCG_THREADS="256", DOT_COCG_SMEM_KB="110"),
-         # z-register pass: every thread-count option, ring depth, tile height and clusters
-         dict(DOT_COCG_ZOPT="A"), dict(DOT_COCG_ZOPT="B"), dict(DOT_COCG_ZOPT="C"),
-         dict(DOT_COCG_PREFETCH="1"), dict(DOT_COCG_PREFETCH="3"), dict(DOT_COCG_TY="3"), dict(DOT_COCG_TY="5"),
-         dict(DOT_COCG_TY="4", DOT_COCG_CLUSTER="2"), dict(DOT_COCG_ZOPT="D"),
-         dict(DOT_COCG_ZOPT="D", DOT_COCG_TY="5"), dict(DOT_COCG_ZOPT="D", DOT_COCG_TY="3", DOT_COCG_PREFETCH="1"),
-]
+KNOBS = [dict(DOT_CG_ROWS="1"), dict(DOT_CG_ROWS="2"),
+         dict(DOT_CG_PREFETCH="1"), dict(DOT_CG_PREFETCH="3"), dict(DOT_CG_TY="3"), dict(DOT_CG_TY="5"),
+         dict(DOT_CG_ROWS="1", DOT_CG_TY="4"), dict(DOT_CG_ROWS="2", DOT_CG_TY="3", DOT_CG_PREFETCH="1"),
+         ]
 
 
 @pytest.mark.parametrize("knobs", KNOBS)
@@ -372,10 +366,10 @@ def test_random_geometries_and_tilings(dot, seed, monkeypatch):
     random z-pass tiling option: dense solves and sampled measurements vs the oracle."""
     rng = np.random.default_rng(1000 + seed)
     nx, ny, nz = int(rng.integers(3, 40)), int(rng.integers(3, 40)), int(rng.integers(2, 30))
-    opt = ["A", "B", "C", "D", "E", "F", "G"][seed % 7]
-    monkeypatch.setenv("DOT_COCG_ZOPT", opt)
+    opt = ["1", "2"][seed % 2]
+    monkeypatch.setenv("DOT_CG_ROWS", opt)
     if seed % 3 == 0 and nz >= 8:
-        monkeypatch.setenv("DOT_COCG_ZCHUNKS", str(int(rng.integers(2, 5))))
+        monkeypatch.setenv("DOT_CG_ZCHUNKS", str(int(rng.integers(2, 5))))
     L = (float(rng.uniform(1.5, 4.0)), float(rng.uniform(1.5, 4.0)), float(rng.uniform(1.0, 3.0)))
     src = (min(2, nx), min(2, ny))
     det = (min(2, nx), min(3, ny))
