@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="one untimed step (for ncu launch lists)")
+    ap.add_argument("--oracle-sample", default=None, help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -156,11 +157,37 @@ def oracle_sample(cfg_name, n_rhs=8, freq=0):
     return value, sample, {"t_factor_s": t_factor, "t_solve_per_rhs_s": t_solve}
 
 
-def cpu_baseline_worker(cfg_name, out_path):
-    """Runs the CPU oracle on a bounded sample (separate process, rank 0 only)."""
+SINGLE_THREAD_ENV = {"OMP_NUM_THREADS": "1", "OPENBLAS_NUM_THREADS": "1", "MKL_NUM_THREADS": "1",
+                     "VECLIB_MAXIMUM_THREADS": "1", "NUMEXPR_NUM_THREADS": "1"}
+
+
+def pinned_cmd(argv):
+    """argv under `taskset -c <one core>` when taskset exists (the core the process may use)."""
+    import shutil
+    core = min(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else 0
+    if shutil.which("taskset"):
+        return ["taskset", "-c", str(core)] + argv, 1
+    return argv, 1
+
+
+def run_cpu_baseline(cfg_name):
+    """The CPU oracle on a bounded sample, alone (nothing else of this run is executing),
+    in a child pinned to ONE core with single-threaded BLAS/OpenMP.  Returns the
+    cpu_baseline object."""
+    cmd, cores = pinned_cmd([sys.executable, os.path.abspath(__file__), "--oracle-sample", cfg_name])
+    env = dict(os.environ, **SINGLE_THREAD_ENV)
+    r = subprocess.run(cmd, env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, timeout=1800)
+    if r.returncode != 0:
+        return {"unavailable": r.stderr.strip().splitlines()[-1] if r.stderr.strip() else "oracle sample failed"}
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    out.update({"unit": UNIT, "cores": cores, "kind": "oracle",
+                "pinning": "taskset -c <1 core>, OMP/OPENBLAS/MKL_NUM_THREADS=1, run before the GPU warm-up"})
+    return out
+
+
+def oracle_sample_main(cfg_name):
     value, sample, detail = oracle_sample(cfg_name)
-    json.dump({"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample, **detail},
-              open(out_path, "w"))
+    print(json.dumps({"value": value, "sample": sample, **detail}), flush=True)
 
 
 # ------------------------------------------------------------------ reference arm
@@ -170,6 +197,10 @@ def run_reference(args, rank, world):
     only; other ranks exit without work."""
     if rank != 0:
         return
+    # same conditions as the main arm's cpu_baseline: one core, single-threaded BLAS / OpenMP
+    os.environ.update(SINGLE_THREAD_ENV)
+    if hasattr(os, "sched_setaffinity"):
+        os.sched_setaffinity(0, {min(os.sched_getaffinity(0))})
     from synth import config_by_name
     cfg = config_by_name(args.config)
     times, vals, sample = [], [], ""
@@ -195,6 +226,9 @@ def run_reference(args, rank, world):
 # ------------------------------------------------------------------ our arm
 def main():
     args = parse()
+    if args.oracle_sample:
+        oracle_sample_main(args.oracle_sample)
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -223,14 +257,11 @@ def main():
     wl = make_workload(cfg)
     dev = torch.device("cuda", local)
 
-    # cpu baseline in a separate process, overlapping the GPU timing (rank 0, N = 1)
-    cpu_proc = None
-    cpu_out = os.path.join("/tmp", f"dot_cpu_baseline_{os.getpid()}.json")
+    # cpu baseline: the oracle sample runs alone, BEFORE any GPU work (rank 0, N = 1), in a
+    # child process pinned to one core with single-threaded BLAS / OpenMP
+    cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
-        import multiprocessing as mp
-        ctx = mp.get_context("spawn")
-        cpu_proc = ctx.Process(target=cpu_baseline_worker, args=(args.config, cpu_out))
-        cpu_proc.start()
+        cpu = run_cpu_baseline(args.config)
 
     # synthetic data: forward model at the hidden level set + 1% noise (setup, untimed;
     # computed by the GPU path because the oracle's LU at 64^3 takes minutes -- the
@@ -407,18 +438,14 @@ def main():
     traffic = ncu_traffic()
     roof = {"bound": "hbm", "kernel": "cocg_zpass_kernel", "achieved": gbs, "peak": peak, "unit": "GB/s",
             "frac": gbs / peak, "peak_source": peak_src,
-            "algorithmic_bytes": "64 B per grid point per COCG iteration per RHS (read r_k, p_k-1; write r_k+1, p_k)",
+            "algorithmic_bytes": ("32 B per grid point per CG iteration per real seed (read r_k, p_k-1; write "
+                                  "r_k+1, p_k in fp64); one seed delivers every frequency (multi-shift CG)"),
             "traffic": traffic["dram_bytes"] if traffic else None,
             "traffic_algorithmic": traffic["algorithmic_bytes_if_all_active"] if traffic else None,
             "traffic_ratio": traffic["ratio"] if traffic else None,
             "traffic_note": traffic["note"] if traffic else "no ncu --set full capture committed yet"}
     jf = st["contract_flops"] / max(st["contract_ms"], 1e-9) / 1e9
     fpk, fsrc = fp64_peak()
-    cpu = None
-    if cpu_proc is not None:
-        cpu_proc.join(timeout=1800)
-        if os.path.exists(cpu_out):
-            cpu = json.load(open(cpu_out))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -430,6 +457,8 @@ def main():
                           else f"working set ~{ws_bytes / 1e6:.0f} MB: 256 MB L2 flush between timed steps"),
                    "cocg_tol": 1e-17},
         "krylov_iterations_per_s": (st["rhs_iterations"] - s0["rhs_iterations"]) / args.steps / (ms / 1e3),
+        "seed_solves_per_step": (st["seeds_solved"] - s0["seeds_solved"]) / args.steps,
+        "seed_iterations_per_s": (st["seed_iterations"] - s0["seed_iterations"]) / args.steps / (ms / 1e3),
         "mean_iters_per_solve": (st["rhs_iterations"] - s0["rhs_iterations"]) / max(st["rhs_solved"] - s0["rhs_solved"], 1),
         "roofline": roof,
         "jacobian": {"path": "block-sparse by basis (default)" if st["contract_flops"] < st["contract_flops_dense"]
@@ -442,6 +471,7 @@ def main():
                      "note": ("block-sparse by basis (PAPER.md L972): useful flops = 4 per (pair, point, parameter) "
                               "with a nonzero dA/dp block; dense_equivalent counts the K x n_p GEMM it replaces")},
         "cpu_baseline": cpu,
+        "solver": "multi-shift CG: one real seed per (source|detector) column serves all n_freq frequencies",
         "e2e": e2e,
         "gpu_launches": int(st["kernel_launches"] - s0["kernel_launches"]),
         "clocks": clocks,

@@ -29,6 +29,10 @@ class DotConfig(C.Structure):
     ]
 
 
+class DotTransport(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("sendrecv", C.c_void_p), ("allreduce_sum", C.c_void_p)]
+
+
 class DotStats(C.Structure):
     _fields_ = [
         ("rhs_solved", C.c_int64), ("rhs_iterations", C.c_int64),
@@ -68,6 +72,7 @@ SIGNATURES = {
                                                    C.c_int, C.c_void_p, C.c_void_p, dp]),
     "dot_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "dot_dd_create": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "dot_dd_create_transport": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]),
     "dot_dd_fields": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int]),
     "dot_dd_last_error": (C.c_char_p, [C.c_void_p]),
     "dot_dd_destroy": (C.c_int, [C.c_void_p]),

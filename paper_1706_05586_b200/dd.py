@@ -1,11 +1,14 @@
-"""z-slab domain decomposition of the batched COCG solves (thin binding of the
+"""z-slab domain decomposition of the batched multi-shift CG solves (thin binding of the
 dot_dd_* calls of include/dot_b200.h).
 
-Two layouts, both running the same library code path:
+Three layouts, all running the same library code path:
   * LocalDD(problems): all ranks in this process (single-GPU emulation: the halo
-    exchange and the all-reduce of the Krylov partial sums are device copies);
+    exchange and the sum of the Krylov partials are device copies);
   * NcclDD(problem, rank, world): one rank per process/GPU, NCCL for the exchange;
-    the NCCL id travels over the caller's torch.distributed group.
+    the NCCL id travels over the caller's torch.distributed group;
+  * TransportDD(problem, rank, world): one rank per process, the library's packed
+    halo buffers and partial sums staged through host memory and exchanged by
+    torch.distributed point-to-point / all_reduce on the caller's group (gloo).
 After `fields(W, V)` every rank's problem has the forward fields of B W and the
 adjoint fields of C V cached, and misfit / jacobian run without further solves.
 """
@@ -20,9 +23,18 @@ from ._abi import DotError
 
 
 class _DD:
-    def __init__(self, problems, rank0, world, nccl_id=None):
+    def __init__(self, problems, rank0, world, nccl_id=None, transport=None):
         self._lib = _abi.load()
         self.problems = list(problems)
+        if transport is not None:
+            h = C.c_void_p()
+            self._transport = transport
+            code = self._lib.dot_dd_create_transport(self.problems[0]._h, int(rank0), int(world),
+                                                     C.byref(transport.struct), C.byref(h))
+            if code:
+                raise DotError(code, (self._lib.dot_dd_last_error(None) or b"").decode())
+            self._h = h
+            return
         arr = (C.c_void_p * len(self.problems))(*[p._h.value for p in self.problems])
         h = C.c_void_p()
         idp = None
@@ -86,6 +98,63 @@ def broadcast_unique_id(rank: int, group=None) -> bytes:
     obj = [nccl_unique_id() if rank == 0 else None]
     tdist.broadcast_object_list(obj, src=0, group=group)
     return obj[0]
+
+
+class TorchTransport:
+    """dot_transport callbacks over a torch.distributed group (CPU tensors: gloo).
+
+    sendrecv(peer, send, recv): isend of the library's host send buffer and irecv into its
+    receive buffer (both posted before waiting, so neighbour chains cannot deadlock);
+    allreduce_sum(buf, n): in-place all_reduce of n doubles.  Argument marshalling only."""
+
+    SENDRECV = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t)
+    ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t)
+
+    def __init__(self, group=None):
+        self.group = group
+        self.errors = []
+        self._sr = self.SENDRECV(self._sendrecv)
+        self._ar = self.ALLREDUCE(self._allreduce)
+        self.struct = _abi.DotTransport(None, C.cast(self._sr, C.c_void_p), C.cast(self._ar, C.c_void_p))
+
+    @staticmethod
+    def _view(addr, nbytes, dtype):
+        import torch
+        return torch.frombuffer((C.c_char * nbytes).from_address(addr), dtype=dtype)
+
+    def _sendrecv(self, ctx, peer, send, send_bytes, recv, recv_bytes):
+        import torch
+        import torch.distributed as tdist
+        try:
+            reqs = []
+            if send_bytes:
+                reqs.append(tdist.isend(self._view(send, send_bytes, torch.uint8), int(peer), group=self.group))
+            if recv_bytes:
+                reqs.append(tdist.irecv(self._view(recv, recv_bytes, torch.uint8), int(peer), group=self.group))
+            for r in reqs:
+                r.wait()
+            return 0
+        except Exception as e:          # reported to the library as a failed exchange
+            self.errors.append(repr(e))
+            return 1
+
+    def _allreduce(self, ctx, buf, n):
+        import torch
+        import torch.distributed as tdist
+        try:
+            if n:
+                tdist.all_reduce(self._view(buf, 8 * n, torch.float64), group=self.group)
+            return 0
+        except Exception as e:
+            self.errors.append(repr(e))
+            return 1
+
+
+class TransportDD(_DD):
+    """One rank per process, exchanged through torch.distributed (e.g. gloo) on `group`."""
+
+    def __init__(self, problem, rank, world, group=None):
+        super().__init__([problem], rank, world, transport=TorchTransport(group))
 
 
 class NcclDD(_DD):

@@ -99,3 +99,77 @@ def test_dd_rejects_too_many_ranks(dot):
     with pytest.raises(DotError):
         dd.fields(None, None)
     dd.close()
+
+
+def _gloo_dd_worker(rank, world, port, ci, q):
+    """One rank per process (the nlocal == 1 branch of dd_solve), halo planes and partial
+    sums exchanged through torch.distributed on gloo (host-staged dot_transport).  All ranks
+    share the one GPU of the box; no kernel waits on another rank (the exchange is a host
+    call between passes)."""
+    import os
+    try:
+        import torch
+        import torch.distributed as tdist
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        tdist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        import paper_1706_05586_b200 as dot
+        from paper_1706_05586_b200.dd import TransportDD
+        cfg = small_config(**CASES[ci], eps=0.4)
+        prob, wl = small_problem(cfg, with_data=True)
+        rng = np.random.default_rng(world)
+        W = np.sign(rng.standard_normal((cfg.n_s, 3)))
+        V = np.sign(rng.standard_normal((cfg.n_d, 2)))
+        g = dot.DOTProblem.from_config(cfg, wl.src_nodes, wl.det_nodes)
+        g.set_data(prob.data)
+        g.set_params(wl.p)
+        g.reset_stats()
+        dd = TransportDD(g, rank, world)
+        dd.fields(W, V)
+        solved = g.stats()["rhs_solved"]
+        m, J = g.misfit(W, V), g.jacobian(W, V)
+        q.put(("ok", rank, m, J, solved, g.stats()["rhs_solved"]))
+        dd.close()
+        tdist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        import traceback
+        q.put(("error", rank, traceback.format_exc(), None, 0, 0))
+
+
+@pytest.mark.parametrize("ci,world", [(0, 2), (1, 2), (0, 3)])
+def test_transport_dd_multiprocess_gloo_matches_oracle(dot, ci, world):
+    """world ranks as separate processes, exchanged over gloo through the library's
+    host-staged transport: misfit within 1e-8 and J within 1e-7 of the oracle
+    (north_star), identical on every rank."""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_dd_worker, args=(r, world, port, ci, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r = q.get(timeout=600)
+        res[r[1]] = r
+    for p in procs:
+        p.join(timeout=120)
+    for r in res.values():
+        assert r[0] == "ok", r[2]
+    cfg = small_config(**CASES[ci], eps=0.4)
+    prob, wl = small_problem(cfg, with_data=True)
+    rng = np.random.default_rng(world)
+    W = np.sign(rng.standard_normal((cfg.n_s, 3)))
+    V = np.sign(rng.standard_normal((cfg.n_d, 2)))
+    m_or, J_or = misfit(prob, wl.p, W, V), jacobian(prob, wl.p, W, V)
+    nf = len(cfg.freqs_hz)
+    for rank, (_, _, m, J, solved, solved_after) in res.items():
+        assert solved == nf * (3 + 2) and solved_after == solved
+        assert abs(m - m_or) <= 1e-8 * m_or, (rank, m, m_or)
+        assert rel(J, J_or) <= 1e-7, rank
+    assert abs(res[0][2] - res[world - 1][2]) <= 1e-12 * res[0][2]

@@ -1,6 +1,6 @@
 #!/bin/bash
 # One GPU round: smoke, GPU parity suite, default bench line, ncu launch list of a
-# short bench, ncu --set full of the COCG pass and the Jacobian contraction.
+# short bench, ncu --set full of the CG pass and the Jacobian contraction.
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/nvsmi.txt 2>&1
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
@@ -14,7 +14,7 @@ PCMD="python bench.py --profile --no-cpu-baseline --no-e2e"
 timeout 600 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 600 $PCMD > gpurun_out/plain2.log 2>&1 && \
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:cocg_zpass -s 60 -c 1 -o gpurun_out/prof_pass $PCMD > gpurun_out/ncu_pass.log 2>&1; echo "ncu pass rc=$?"
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:cg_pass_kernel -s 60 -c 1 -o gpurun_out/prof_pass $PCMD > gpurun_out/ncu_pass.log 2>&1; echo "ncu pass rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:contract -c 2 -o gpurun_out/prof_contract $PCMD > gpurun_out/ncu_contract.log 2>&1; echo "ncu contract rc=$?"
 python tools/sass_mix.py gpurun_out/prof_pass.ncu-rep > gpurun_out/sass_mix.txt 2>&1
 ls -la gpurun_out

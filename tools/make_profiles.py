@@ -47,7 +47,7 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active"]
 traffic = None
-for rep, name in (("prof_pass", "cocg_zpass"), ("prof_contract", "contract")):
+for rep, name in (("prof_pass", "cg_pass"), ("prof_contract", "contract")):
     path = os.path.join(G, rep + ".ncu-rep")
     if not os.path.exists(path):
         continue
@@ -65,16 +65,16 @@ for rep, name in (("prof_pass", "cocg_zpass"), ("prof_contract", "contract")):
                      and k.endswith("per_issue_active.ratio") and v[k] not in ("", "n/a")), reverse=True)
         for val, k in st[:8]:
             lines.append(f"  stall {k.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')} = {val:.3f}")
-        if name == "cocg_zpass" and traffic is None:
+        if name == "cg_pass" and traffic is None:
             gx, gy = [int(t) for t in v["Grid Size"].strip("()").split(",")[:2]]
             rd = float(v["dram__bytes_read.sum"]); wr = float(v["dram__bytes_write.sum"])
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             rd *= scale[units[hh.index("dram__bytes_read.sum")]]
             wr *= scale[units[hh.index("dram__bytes_write.sum")]]
-            traffic = {"launch_rhs": gy, "grid": [gx, gy], "dram_bytes": rd + wr,
+            traffic = {"launch_pairs": gy, "grid": [gx, gy], "dram_bytes": rd + wr,
                        "algorithmic_bytes_if_all_active": 64.0 * 64 ** 3 * gy,
-                       "note": (f"ncu --set full capture of one cocg_zpass_kernel launch ({gy} RHS, 64^3) in "
-                                f"bench.py --profile: dram read+write per launch vs 64 B/point/RHS algorithmic")}
+                       "note": (f"ncu --set full capture of one cg_pass_kernel launch ({gy} seed pairs, 64^3) in "
+                                f"bench.py --profile: dram read+write per launch vs 32 B/point/seed algorithmic")}
             traffic["ratio"] = traffic["dram_bytes"] / traffic["algorithmic_bytes_if_all_active"]
     with open(os.path.join(P, f"{tag}_ncu_{name}.txt"), "w") as fo:
         fo.write(f"# ncu --set full --clock-control none --import-source on ({rep}.ncu-rep), bench.py --profile\n")
@@ -84,7 +84,7 @@ if traffic:
     json.dump(traffic, open(os.path.join(P, "cocg_pass_traffic.json"), "w"), indent=1)
     print(traffic)
 if os.path.exists(os.path.join(G, "sass_mix.txt")):
-    shutil.copy(os.path.join(G, "sass_mix.txt"), os.path.join(P, f"{tag}_ncu_cocg_zpass_sass_mix.txt"))
+    shutil.copy(os.path.join(G, "sass_mix.txt"), os.path.join(P, f"{tag}_ncu_cg_pass_sass_mix.txt"))
 bl = [l for l in open(os.path.join(G, "bench.log")) if l.startswith("{")]
 if bl:
     open(os.path.join(P, f"{tag}_bench.jsonl"), "w").write(bl[-1])
