@@ -101,7 +101,7 @@ def test_dd_rejects_too_many_ranks(dot):
     dd.close()
 
 
-def _gloo_dd_worker(rank, world, port, ci, q):
+def _gloo_dd_worker(rank, world, port, ci, data, q):
     """One rank per process (the nlocal == 1 branch of dd_solve), halo planes and partial
     sums exchanged through torch.distributed on gloo (host-staged dot_transport).  All ranks
     share the one GPU of the box; no kernel waits on another rank (the exchange is a host
@@ -115,13 +115,15 @@ def _gloo_dd_worker(rank, world, port, ci, q):
         torch.cuda.set_device(0)
         import paper_1706_05586_b200 as dot
         from paper_1706_05586_b200.dd import TransportDD
+        from synth import make_workload
         cfg = small_config(**CASES[ci], eps=0.4)
-        prob, wl = small_problem(cfg, with_data=True)
+        wl = make_workload(cfg)                 # the seeded inputs of small_problem (no oracle here)
+        wl.p[0] = max(wl.p[0], 0.8)
         rng = np.random.default_rng(world)
         W = np.sign(rng.standard_normal((cfg.n_s, 3)))
         V = np.sign(rng.standard_normal((cfg.n_d, 2)))
         g = dot.DOTProblem.from_config(cfg, wl.src_nodes, wl.det_nodes)
-        g.set_data(prob.data)
+        g.set_data(data)
         g.set_params(wl.p)
         g.reset_stats()
         dd = TransportDD(g, rank, world)
@@ -148,9 +150,11 @@ def test_transport_dd_multiprocess_gloo_matches_oracle(dot, ci, world):
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
+    cfg = small_config(**CASES[ci], eps=0.4)
+    prob, wl = small_problem(cfg, with_data=True)     # oracle data in the parent only
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_gloo_dd_worker, args=(r, world, port, ci, q)) for r in range(world)]
+    procs = [ctx.Process(target=_gloo_dd_worker, args=(r, world, port, ci, prob.data, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -161,8 +165,6 @@ def test_transport_dd_multiprocess_gloo_matches_oracle(dot, ci, world):
         p.join(timeout=120)
     for r in res.values():
         assert r[0] == "ok", r[2]
-    cfg = small_config(**CASES[ci], eps=0.4)
-    prob, wl = small_problem(cfg, with_data=True)
     rng = np.random.default_rng(world)
     W = np.sign(rng.standard_normal((cfg.n_s, 3)))
     V = np.sign(rng.standard_normal((cfg.n_d, 2)))
