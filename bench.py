@@ -120,7 +120,7 @@ def fp64_peak():
 
 
 def ncu_traffic():
-    path = os.path.join(ROOT, "profiles", "cocg_pass_traffic.json")
+    path = os.path.join(ROOT, "profiles", "cg_pass_traffic.json")
     if os.path.exists(path):
         return json.load(open(path))
     return None
@@ -282,27 +282,18 @@ def main():
     V_d = torch.as_tensor(wl.V, device=dev) if wl.V is not None else None
     D_d = torch.as_tensor(data, device=dev)
 
-    if cfg.name == "full64":
+    if cfg.name in ("full64", "all128"):
         def run_step(p, W, V, data=None):
+            """configs[2] (full64) / configs[4] (all128): set_params, all n_s forward and n_d
+            adjoint fields at every frequency (multi-shift seeds, RHS-sharded over the ranks),
+            full-data misfit, the FULL Jacobian (gathered on
+            rank 0) and, when the config has a sketch, (W^T (x) V^T) J."""
             return sharded_step(gp, plan, p, W, V, data=data,
                                 comm_device=None if backend_name == "nccl" else torch.device("cpu"))
-    elif cfg.name == "all128":
-        if world > 1:
-            raise SystemExit("bench: all128 runs single-GPU here")
-
-        def run_step(p, W, V, data=None):
-            """configs[4] (all128) solve part: set_params, all 1024 x 5 forward and 1024 x 5
-            adjoint solves in chunked batches, all-sources misfit.  The full Jacobian
-            contraction (~1e17 flop at |S| ~ 3e4) is not part of this row."""
-            if data is not None:
-                gp.set_data(data)
-            gp.set_params(p)
-            gp.prefetch_fields(None, None)
-            m = gp.misfit(None, None)
-            return {"misfit": m, "d2h_bytes": 8}
     else:
         if world > 1:
-            raise SystemExit("bench: only the full64 workload shards over ranks (others are single-GPU rows)")
+            raise SystemExit("bench: the full64 and all128 workloads shard over ranks; sketch32 / opt96 are "
+                             "single-GPU rows")
         X0s = torch.as_tensor(wl.X0_src, device=dev) if wl.X0_src is not None else None
         X0d = torch.as_tensor(wl.X0_det, device=dev) if wl.X0_det is not None else None
 
@@ -372,7 +363,7 @@ def main():
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         ms = float(t.item())
     solves_per_step = (st["rhs_solved"] - s0["rhs_solved"]) / args.steps     # counted by the library
-    if cfg.name == "full64":
+    if cfg.name in ("full64", "all128"):
         solves_per_step = cfg.n_freq * (cfg.n_s + cfg.n_d)                     # per step, all ranks
     value = solves_per_step / (ms / 1e3)
 
@@ -436,7 +427,7 @@ def main():
     peak, peak_src = measured_peaks()
     gbs = (st["pass_bytes"] - s0["pass_bytes"]) / max(st["pass_ms"] - s0["pass_ms"], 1e-9) / 1e6
     traffic = ncu_traffic()
-    roof = {"bound": "hbm", "kernel": "cocg_zpass_kernel", "achieved": gbs, "peak": peak, "unit": "GB/s",
+    roof = {"bound": "hbm", "kernel": "cg_pass_kernel", "achieved": gbs, "peak": peak, "unit": "GB/s",
             "frac": gbs / peak, "peak_source": peak_src,
             "algorithmic_bytes": ("32 B per grid point per CG iteration per real seed (read r_k, p_k-1; write "
                                   "r_k+1, p_k in fp64); one seed delivers every frequency (multi-shift CG)"),

@@ -223,7 +223,13 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, c
     const size_t ppb = per_pair_bytes(P, nP, hist, nsl);
     size_t fit = P->arena.largest_free() / ppb;
     fit = fit > 2 ? fit - 1 : fit;      // several allocations fragment the arena: keep a margin
-    if (fit < 1) throw Error(DOT_ERR_WORKSPACE, "workspace too small for one pair of right-hand sides");
+    if (fit < 1)
+        throw Error(DOT_ERR_WORKSPACE, "workspace too small for one pair of right-hand sides (pair needs " +
+                                           std::to_string(ppb) + " B, largest free block " +
+                                           std::to_string(P->arena.largest_free()) + " B of " +
+                                           std::to_string(P->arena.capacity()) + " B, " +
+                                           std::to_string(P->arena.used_bytes()) + " B in use; nP " +
+                                           std::to_string(nP) + ", N " + std::to_string(N) + ")");
     const int chunk = (int)std::min<size_t>(fit, (size_t)npairs);
     const int CHK = 8;
     // z chunks: enough CTAs to fill the GPU when few pairs iterate together on a deep grid

@@ -62,6 +62,12 @@ public:
         free_[off] = len;
     }
 
+    size_t capacity() const { return size_; }
+    size_t used_bytes() const {
+        size_t u = 0;
+        for (const auto& kv : used_) u += kv.second;
+        return u;
+    }
     size_t largest_free() const {
         size_t m = 0;
         for (auto& kv : free_) m = kv.second > m ? kv.second : m;

@@ -32,9 +32,9 @@ class ShardPlan:
 
     @staticmethod
     def _block(n, world, r):
-        per = (n + world - 1) // world
-        lo = min(r * per, n)
-        return lo, min(lo + per, n)
+        """Balanced contiguous split: block sizes differ by at most one (a rank may own
+        nothing when n < world)."""
+        return r * n // world, (r + 1) * n // world
 
     @property
     def per_src(self):
@@ -80,19 +80,20 @@ def _as_dev(x, like):
 
 def sharded_step(backend, plan: ShardPlan, p, W, V, data=None, device=None, comm_device=None):
     """One step: set_params, all-source + all-detector solves, full-data misfit,
-    full Jacobian and the sketched Jacobian (W, V).  Returns a dict with
-    misfit, J_full (rank 0), J_sketch, d2h_bytes."""
+    full Jacobian and (when W or V is given) the sketched Jacobian (W, V).  Returns a
+    dict with misfit, J_full (rank 0), J_sketch, d2h_bytes."""
     torch = _torch()
     host_io = not (isinstance(p, torch.Tensor) and p.is_cuda)
+    sketch = W is not None or V is not None
     if data is not None:
         backend.set_data(data)
     backend.set_params(p)
     if plan.world == 1:
         where = 0 if host_io else 1
-        J_full = backend.jacobian(None, None, where=where)          # 1536 solves + full J (DMMA)
+        J_full = backend.jacobian(None, None, where=where)          # all solves + full J (DMMA)
         m = backend.misfit(None, None)                                # cached forward fields
-        J_sk = backend.jacobian(W, V)                                 # by combination of cached fields
-        d2h = (J_full.nbytes + J_sk.nbytes + 8) if host_io else 0
+        J_sk = backend.jacobian(W, V) if sketch else None             # by combination of cached fields
+        d2h = (J_full.nbytes + (J_sk.nbytes if sketch else 0) + 8) if host_io else 0
         return {"misfit": m, "J_full": J_full, "J_sketch": J_sk, "d2h_bytes": d2h}
 
     import torch.distributed as tdist
@@ -114,15 +115,18 @@ def sharded_step(backend, plan: ShardPlan, p, W, V, data=None, device=None, comm
 
     slo, shi = plan.src_block()
     dlo, dhi = plan.det_block()
-    Wn = W.detach().cpu().numpy() if isinstance(W, torch.Tensor) else np.asarray(W)
-    Vn = V.detach().cpu().numpy() if isinstance(V, torch.Tensor) else np.asarray(V)
     Es = _as_dev(selection(plan.n_s, slo, shi), torch.empty(0, device=dev))
     Ed = _as_dev(selection(plan.n_d, dlo, dhi), torch.empty(0, device=dev))
-    Wm = np.zeros_like(Wn)
-    Wm[slo:shi] = Wn[slo:shi]
-    Vm = np.zeros_like(Vn)
-    Vm[dlo:dhi] = Vn[dlo:dhi]
-    Wm, Vm = _as_dev(Wm, Es), _as_dev(Vm, Es)
+    if sketch:
+        Wn = np.eye(plan.n_s) if W is None else (W.detach().cpu().numpy() if isinstance(W, torch.Tensor)
+                                                  else np.asarray(W))
+        Vn = np.eye(plan.n_d) if V is None else (V.detach().cpu().numpy() if isinstance(V, torch.Tensor)
+                                                  else np.asarray(V))
+        Wm = np.zeros_like(Wn)
+        Wm[slo:shi] = Wn[slo:shi]
+        Vm = np.zeros_like(Vn)
+        Vm[dlo:dhi] = Vn[dlo:dhi]
+        Wm, Vm = _as_dev(Wm, Es), _as_dev(Vm, Es)
 
     # forward solves of my source block and adjoint solves of my detector block, one batch
     if hasattr(backend, "prefetch_fields"):
@@ -132,16 +136,25 @@ def sharded_step(backend, plan: ShardPlan, p, W, V, data=None, device=None, comm
     m_part = backend.misfit(Es, None) if shi > slo else 0.0
     m = torch.tensor([m_part], dtype=torch.float64, device=dev)
     all_reduce_(m)
-    # sampled fields of my blocks on S (cached from the solves)
-    U_blk = T(backend.fields_on_support(0, Es))       # [nf][ns_r][K]
-    L_blk = T(backend.fields_on_support(1, Ed))       # [nf][nd_r][K]
-    # sketched fields: partial combinations of my blocks, summed over ranks
-    UW = T(backend.fields_on_support(0, Wm))
-    LV = T(backend.fields_on_support(1, Vm))
-    for t in (UW, LV):
-        all_reduce_(t)
+    # sampled fields of my blocks on S (cached from the solves); an empty block contributes
+    # a zero-width panel
     G = T(backend.support_weights())
-    J_sk = T(backend.contract(LV, UW, G))
+    K = G.shape[0]
+
+    def fields(side, E, nonempty):
+        if nonempty:
+            return T(backend.fields_on_support(side, E))
+        return torch.zeros((backend.n_freq, 0, K), dtype=torch.complex128, device=dev)
+    U_blk = fields(0, Es, shi > slo)                  # [nf][ns_r][K]
+    L_blk = fields(1, Ed, dhi > dlo)                  # [nf][nd_r][K]
+    J_sk = None
+    if sketch:
+        # sketched fields: partial combinations of my blocks, summed over ranks
+        UW = T(backend.fields_on_support(0, Wm))
+        LV = T(backend.fields_on_support(1, Vm))
+        for t in (UW, LV):
+            all_reduce_(t)
+        J_sk = T(backend.contract(LV, UW, G))
     # full Jacobian: every source field on S to every rank, rows of my detector block
     nf, K = U_blk.shape[0], U_blk.shape[2]
     pad = torch.zeros((nf, plan.per_src, K), dtype=U_blk.dtype, device=cdev)
@@ -161,8 +174,10 @@ def sharded_step(backend, plan: ShardPlan, p, W, V, data=None, device=None, comm
                             for r in range(plan.world)], 1)
     d2h = 0
     if host_io:
-        J_sk = J_sk.cpu().numpy()
-        d2h += J_sk.nbytes + 8
+        d2h += 8
+        if J_sk is not None:
+            J_sk = J_sk.cpu().numpy()
+            d2h += J_sk.nbytes
         if J_full is not None:
             J_full = J_full.cpu().numpy()
             d2h += J_full.nbytes

@@ -1,7 +1,8 @@
 """The RHS-sharded step (paper_1706_05586_b200/sharded.py) with world_size 2 on ONE GPU:
 two processes, each a rank with its own DOTProblem on cuda:0, collectives over gloo
 (the ranks' kernels never wait on each other -- all exchange happens between calls).
-Must equal the unsharded step: misfit, full Jacobian (rank 0) and sketched Jacobian."""
+Checked against the CPU oracle (misfit 1e-8, Jacobians 1e-7; north_star) and against
+the unsharded GPU step."""
 import os
 import socket
 
@@ -82,6 +83,14 @@ def test_two_rank_sharded_step_on_one_gpu():
     rng = np.random.default_rng(0)
     W = np.sign(rng.standard_normal((cfg.n_s, 3)))
     V = np.sign(rng.standard_normal((cfg.n_d, 2)))
+    from oracle import jacobian, misfit
+    m_or = misfit(prob, wl.p, np.eye(cfg.n_s), np.eye(cfg.n_d))
+    Jf_or = jacobian(prob, wl.p, np.eye(cfg.n_s), np.eye(cfg.n_d))
+    Js_or = jacobian(prob, wl.p, W, V)
+    for r in res:
+        assert abs(r["misfit"] - m_or) <= 1e-8 * m_or
+        assert np.linalg.norm(r["J_sketch"] - Js_or) <= 1e-7 * np.linalg.norm(Js_or)
+    assert np.linalg.norm(res[0]["J_full"] - Jf_or) <= 1e-7 * np.linalg.norm(Jf_or)
     g = dot.DOTProblem.from_config(cfg, wl.src_nodes, wl.det_nodes)
     ref = sharded_step(g, ShardPlan(0, 1, cfg.n_s, cfg.n_d), wl.p, W, V, data=prob.data)
     for r in res:

@@ -19,6 +19,7 @@ class OracleBackend:
 
     def __init__(self, prob):
         self.prob = prob
+        self.n_freq = len(prob.omegas)
 
     def set_data(self, d):
         self.prob.data = np.asarray(d)
@@ -66,16 +67,21 @@ def _free_port():
     return port
 
 
+CASES = {2: dict(n=(7, 7, 5), src=(3, 1), det=(2, 2), eps=0.4),
+         # world 3 with 2 sources: one rank owns no source column (empty block)
+         3: dict(n=(7, 7, 5), src=(2, 1), det=(2, 2), eps=0.4)}
+
+
 def _worker(rank, world, port, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     tdist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1706_05586_b200.sharded import ShardPlan, sharded_step
-    cfg = small_config(n=(7, 7, 5), src=(3, 1), det=(2, 2), eps=0.4)
+    cfg = small_config(**CASES[world])
     prob, wl = small_problem(cfg)
     rng = np.random.default_rng(0)
-    W = np.sign(rng.standard_normal((3, 2)))
-    V = np.sign(rng.standard_normal((4, 3)))
-    plan = ShardPlan(rank, world, 3, 4)
+    W = np.sign(rng.standard_normal((cfg.n_s, 2)))
+    V = np.sign(rng.standard_normal((cfg.n_d, 3)))
+    plan = ShardPlan(rank, world, cfg.n_s, cfg.n_d)
     try:
         r = sharded_step(OracleBackend(prob), plan, torch.as_tensor(wl.p), torch.as_tensor(W), torch.as_tensor(V),
                          device=torch.device("cpu"))
@@ -90,15 +96,16 @@ def _worker(rank, world, port, out):
     tdist.destroy_process_group()
 
 
-def test_two_rank_sharded_step_equals_unsharded():
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_step_equals_unsharded(world):
     from oracle import jacobian, misfit
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=300) for _ in range(2)]
+    res = [q.get(timeout=300) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -106,13 +113,13 @@ def test_two_rank_sharded_step_equals_unsharded():
     assert not errors, errors
     main = [r for r in res if r[0] != "solves"][0]
     m, Jf, Js, solves0 = main
-    cfg = small_config(n=(7, 7, 5), src=(3, 1), det=(2, 2), eps=0.4)
+    cfg = small_config(**CASES[world])
     prob, wl = small_problem(cfg)
     rng = np.random.default_rng(0)
-    W = np.sign(rng.standard_normal((3, 2)))
-    V = np.sign(rng.standard_normal((4, 3)))
-    assert m == pytest.approx(misfit(prob, wl.p, np.eye(3), np.eye(4)), rel=1e-10)
-    Jf_ref = jacobian(prob, wl.p, np.eye(3), np.eye(4))
+    W = np.sign(rng.standard_normal((cfg.n_s, 2)))
+    V = np.sign(rng.standard_normal((cfg.n_d, 3)))
+    assert m == pytest.approx(misfit(prob, wl.p, np.eye(cfg.n_s), np.eye(cfg.n_d)), rel=1e-10)
+    Jf_ref = jacobian(prob, wl.p, np.eye(cfg.n_s), np.eye(cfg.n_d))
     assert np.abs(Jf - Jf_ref).max() <= 1e-10 * np.abs(Jf_ref).max()
     Js_ref = jacobian(prob, wl.p, W, V)
     assert np.abs(Js - Js_ref).max() <= 1e-10 * np.abs(Js_ref).max()
@@ -120,9 +127,12 @@ def test_two_rank_sharded_step_equals_unsharded():
 
 def test_shard_plan_blocks_cover_once():
     from paper_1706_05586_b200.sharded import ShardPlan
-    for n, w in [(256, 8), (1024, 3), (7, 2), (5, 5)]:
-        covered = []
+    for n, w in [(256, 8), (1024, 3), (7, 2), (5, 5), (12, 8), (2, 3)]:
+        covered, sizes = [], []
         for r in range(w):
             lo, hi = ShardPlan(r, w, n, n).src_block()
             covered.extend(range(lo, hi))
+            sizes.append(hi - lo)
         assert covered == list(range(n))
+        assert max(sizes) - min(sizes) <= 1                  # balanced
+        assert max(sizes) <= ShardPlan(0, w, n, n).per_src  # fits the all_gather padding

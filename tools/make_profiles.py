@@ -81,7 +81,7 @@ for rep, name in (("prof_pass", "cg_pass"), ("prof_contract", "contract")):
         fo.write("\n".join(lines) + "\n")
     print("\n".join(lines))
 if traffic:
-    json.dump(traffic, open(os.path.join(P, "cocg_pass_traffic.json"), "w"), indent=1)
+    json.dump(traffic, open(os.path.join(P, "cg_pass_traffic.json"), "w"), indent=1)
     print(traffic)
 if os.path.exists(os.path.join(G, "sass_mix.txt")):
     shutil.copy(os.path.join(G, "sass_mix.txt"), os.path.join(P, f"{tag}_ncu_cg_pass_sass_mix.txt"))
