@@ -610,50 +610,78 @@ __global__ void __launch_bounds__(256) cg_init_kernel(const PassArgs a, int zc_o
 
 // Fold of passes [k0, k1) into the shifted directions and solutions on the samples
 // [s0, s1): thread (pair, sample) runs both seeds' recurrences in pass order.
+template <int NSL>
 __global__ void __launch_bounds__(128) cg_fold_kernel(FoldArgs f) {
+    // the fold records of this pair's two seeds for passes [k0, k1), valid flags folded in
+    __shared__ double2 sc[2][kHist][NSL][3];      // zeta, beta_sigma, alpha_sigma
+    __shared__ int sv[2][kHist][NSL];
     const int pair = blockIdx.y;
+    const int nk = f.k1 - f.k0, nseeds = 2 * f.npairs;
+    for (int i = threadIdx.x; i < 2 * nk * NSL; i += blockDim.x) {
+        const int e = i / (nk * NSL), rem = i - e * nk * NSL, kk = rem / NSL, sl = rem - kk * NSL;
+        const int seed = 2 * pair + e, k = f.k0 + kk;
+        uint32_t m = f.mask[seed];
+        int q = -1;
+        for (int c = 0; m; ++c) {                  // sl-th needed shift of the seed
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            if (c == sl) {
+                q = b;
+                break;
+            }
+        }
+        int valid = 0;
+        if (q >= 0 && q < f.nshift) {
+            const ShiftCoef c = f.coef[((size_t)(k % f.hist) * nseeds + seed) * kMaxShift + q];
+            valid = (c.k == k && c.active) ? 1 : 0;
+            sc[e][kk][sl][0] = c.zeta;
+            sc[e][kk][sl][1] = c.beta;
+            sc[e][kk][sl][2] = c.alpha;
+        }
+        sv[e][kk][sl] = valid;
+    }
+    __syncthreads();
     const int s = f.s0 + blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= f.s1) return;
-    const int nseeds = 2 * f.npairs;
-#pragma unroll 1
-    for (int e = 0; e < 2; ++e) {
-        const int seed = 2 * pair + e;
-        const uint32_t mask = f.mask[seed];
-        if (!mask) continue;
-        double2 Pv[kMaxShift], Xv[kMaxShift];
+    const uint32_t m0 = f.mask[2 * pair], m1 = f.mask[2 * pair + 1];
+    const int n0 = min(__popc(m0), NSL), n1 = min(__popc(m1), NSL);
+    double2 Pv[2][NSL], Xv[2][NSL];
 #pragma unroll
-        for (int q = 0; q < kMaxShift; ++q) {
-            Pv[q] = cmk(0, 0);
-            Xv[q] = cmk(0, 0);
-            if (q < f.nshift && ((mask >> q) & 1u)) {
-                const size_t ix = ((size_t)seed * f.nsl + __popc(mask & ((1u << q) - 1u))) * f.nP + s;
-                Pv[q] = f.Ps[ix];
-                Xv[q] = f.Xs[ix];
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int sl = 0; sl < NSL; ++sl) {
+            Pv[e][sl] = cmk(0, 0);
+            Xv[e][sl] = cmk(0, 0);
+            if (sl < (e ? n1 : n0)) {
+                const size_t ix = ((size_t)(2 * pair + e) * f.nsl + sl) * f.nP + s;
+                Pv[e][sl] = f.Ps[ix];
+                Xv[e][sl] = f.Xs[ix];
             }
         }
 #pragma unroll 1
-        for (int k = f.k0; k < f.k1; ++k) {
-            const int h = k % f.hist;
-            const double2 hv = f.H[((size_t)h * f.npairs + pair) * f.nP + s];
+    for (int kk = 0; kk < nk; ++kk) {
+        const int k = f.k0 + kk;
+        const double2 hv = f.H[((size_t)(k % f.hist) * f.npairs + pair) * f.nP + s];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
             const double r = e ? hv.y : hv.x;
-            const ShiftCoef* rc = f.coef + ((size_t)h * nseeds + seed) * kMaxShift;
 #pragma unroll
-            for (int q = 0; q < kMaxShift; ++q) {
-                if (q >= f.nshift || !((mask >> q) & 1u)) continue;
-                const ShiftCoef c = rc[q];
-                if (c.k != k || !c.active) continue;
-                Pv[q] = cfma(c.beta, Pv[q], cmul_re(c.zeta, r));
-                Xv[q] = cfma(c.alpha, Pv[q], Xv[q]);
+            for (int sl = 0; sl < NSL; ++sl) {
+                if (!sv[e][kk][sl]) continue;
+                Pv[e][sl] = cfma(sc[e][kk][sl][1], Pv[e][sl], cmul_re(sc[e][kk][sl][0], r));
+                Xv[e][sl] = cfma(sc[e][kk][sl][2], Pv[e][sl], Xv[e][sl]);
             }
         }
-#pragma unroll
-        for (int q = 0; q < kMaxShift; ++q)
-            if (q < f.nshift && ((mask >> q) & 1u)) {
-                const size_t ix = ((size_t)seed * f.nsl + __popc(mask & ((1u << q) - 1u))) * f.nP + s;
-                f.Ps[ix] = Pv[q];
-                f.Xs[ix] = Xv[q];
-            }
     }
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int sl = 0; sl < NSL; ++sl)
+            if (sl < (e ? n1 : n0)) {
+                const size_t ix = ((size_t)(2 * pair + e) * f.nsl + sl) * f.nP + s;
+                f.Ps[ix] = Pv[e][sl];
+                f.Xs[ix] = Xv[e][sl];
+            }
 }
 
 // XP[obase + q*ostride][s] += mul * theta^-1/2 * Xs[seed][q][s] over the seeds' needed shifts
@@ -867,8 +895,19 @@ void launch_cg_init(const PassArgs& a, int nb, cudaStream_t s, int zc_own) {
 
 void launch_cg_fold(const FoldArgs& f, cudaStream_t s) {
     if (f.k1 <= f.k0 || f.s1 <= f.s0 || f.npairs <= 0) return;
+    if (f.k1 - f.k0 > kHist || f.hist > kHist) throw Error(DOT_ERR_ARG, "fold span exceeds the history ring");
     dim3 grid((f.s1 - f.s0 + 127) / 128, f.npairs);
-    cg_fold_kernel<<<grid, 128, 0, s>>>(f);
+    switch (f.nsl) {
+        case 1: cg_fold_kernel<1><<<grid, 128, 0, s>>>(f); break;
+        case 2: cg_fold_kernel<2><<<grid, 128, 0, s>>>(f); break;
+        case 3: cg_fold_kernel<3><<<grid, 128, 0, s>>>(f); break;
+        case 4: cg_fold_kernel<4><<<grid, 128, 0, s>>>(f); break;
+        case 5: cg_fold_kernel<5><<<grid, 128, 0, s>>>(f); break;
+        case 6: cg_fold_kernel<6><<<grid, 128, 0, s>>>(f); break;
+        case 7: cg_fold_kernel<7><<<grid, 128, 0, s>>>(f); break;
+        case 8: cg_fold_kernel<8><<<grid, 128, 0, s>>>(f); break;
+        default: throw Error(DOT_ERR_ARG, "fold: 1..8 shifts per seed");
+    }
     DOT_CUDA_TRY(cudaGetLastError());
 }
 
