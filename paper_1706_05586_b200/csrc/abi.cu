@@ -267,6 +267,7 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, c
         DBuf<int32_t> domap = to_device(P, sp.omap.data() + 3 * s0, 3 * ns, DOT_HOST);
         int nb_launch = nb;
         DOT_CUDA_TRY(cudaMemsetAsync(coef.get(), 0, (size_t)hist * ns * kMaxShift * sizeof(ShiftCoef), P->stream));
+        DOT_CUDA_TRY(cudaMemsetAsync(P0.get(), 0, (size_t)nb * N * sizeof(double2), P->stream));   // p_{-1} = 0
         DOT_CUDA_TRY(cudaMemsetAsync(Ps.get(), 0, (size_t)ns * nsl * std::max(nP, 1) * sizeof(double2), P->stream));
         DOT_CUDA_TRY(cudaMemsetAsync(Xs.get(), 0, (size_t)ns * nsl * std::max(nP, 1) * sizeof(double2), P->stream));
 
@@ -826,6 +827,7 @@ void dd_solve(dot_dd* G, const std::vector<Req>& reqs) {
         }
         cudaStream_t s = P->stream;
         DOT_CUDA_TRY(cudaMemsetAsync(b.R[0].get(), 0, (size_t)nb * N * sizeof(double2), s));
+        DOT_CUDA_TRY(cudaMemsetAsync(b.Pv[0].get(), 0, (size_t)nb * N * sizeof(double2), s));   // p_{-1} = 0
         DOT_CUDA_TRY(cudaMemsetAsync(b.part.get(), 0, 2 * (size_t)nb * nslots * kNumPartials * sizeof(double), s));
         DOT_CUDA_TRY(cudaMemsetAsync(b.coef.get(), 0, (size_t)kHist * ns * kMaxShift * sizeof(ShiftCoef), s));
         DOT_CUDA_TRY(cudaMemsetAsync(b.Ps.get(), 0, (size_t)ns * nf * nPp * sizeof(double2), s));

@@ -230,7 +230,8 @@ struct IC {
 
 // Slot layout (per ring slot): r [rowsP*nx] double2 | p [rowsP*nx] double2 | mu [rowsP*nx] double
 // (mu rides along in the same bulk-copy group when MUT; else it is loaded per thread).
-template <int MAXT, int NS, bool MUT, int RPT, bool ZC>
+// NX_, TY_: compile-time row length and tile height of the bench geometries (0: run time).
+template <int MAXT, int NS, bool MUT, int RPT, bool ZC, int NX_, int TY_>
 __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant__ PassArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int PD = NS - 2;                          // TMA planes in flight
@@ -238,8 +239,8 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
     const int tile = blockIdx.x % ntiles, zc = a.zc0 + blockIdx.x / ntiles;
     const int pair = a.act ? a.act[blockIdx.y] : blockIdx.y;       // active-list compaction (tail passes)
     if (pair < 0) return;                                          // slot past the active count
-    const int nx = a.op.nx, ny = a.op.ny, nz = a.op.nz;
-    const int TY = a.tl.TY;
+    const int nx = NX_ ? NX_ : a.op.nx, ny = a.op.ny, nz = a.op.nz;
+    const int TY = TY_ ? TY_ : a.tl.TY;
     // z chunk [z0, z1) of this CTA; phase 1 runs on [a1, b1), phase 2 on [a2, b2)
     // (two / one halo planes recomputed on each side)
     const int z0 = ZC ? zc * a.zlen : 0, z1 = ZC ? min(nz, z0 + a.zlen) : nz;
@@ -293,8 +294,7 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
     }
     __syncthreads();
     if (!sh_sc.active) return;
-    const bool first = (a.k == 0);
-    const int kin = a.k & 1, kout = kin ^ 1;
+    const int kin = a.k & 1, kout = kin ^ 1;      // pass 0 reads p_{-1} = 0 (zeroed buffer), beta_0 = 0
     const double2* __restrict__ Rin = a.R[kin] + (size_t)pair * N;
     const double2* __restrict__ Pin = a.Pv[kin] + (size_t)pair * N;
     double2* Hk = a.H + ((size_t)(a.k % a.hist) * a.npairs + pair) * a.nP;   // r_k at the samples
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
     const int rlo = max(0, 2 - j0), rhi = min(rowsP, ny - j0 + 2);
     const uint32_t tile_bytes = (uint32_t)((rhi - rlo) * nx * sizeof(double2));
     const uint32_t mu_bytes = tile_bytes / 2;
-    const uint32_t tx_bytes = (first ? tile_bytes : 2 * tile_bytes) + (MUT ? mu_bytes : 0);
+    const uint32_t tx_bytes = 2 * tile_bytes + (MUT ? mu_bytes : 0);
     const int tile_off = (j0 - 2 + rlo) * nx;
     const uint32_t slot0 = smem_u32(slots + rlo * nx);             // r rows of slot 0
     const uint32_t slot_stride = (uint32_t)(slotW * sizeof(double2));
@@ -321,12 +321,11 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dR),
             "l"(Rin + g), "r"(tile_bytes), "r"(bar)
             : "memory");
-        if (!first)
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    dR + pvec_off),
-                "l"(Pin + g), "r"(tile_bytes), "r"(bar)
-                : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                dR + pvec_off),
+            "l"(Pin + g), "r"(tile_bytes), "r"(bar)
+            : "memory");
         if (MUT)
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -421,12 +420,8 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
                     for (int j = 0; j < RPT; ++j) {
                         if (!A && !indom[j]) continue;
                         const double2 rf = sr[j * nx];
-                        if (first) {
-                            pf[j] = rf;
-                        } else {
-                            const double2 pv = sr[slotE + j * nx];
-                            pf[j] = cmk(fma(beta.x, pv.x, rf.x), fma(beta.y, pv.y, rf.y));
-                        }
+                        const double2 pv = sr[slotE + j * nx];
+                        pf[j] = cmk(fma(beta.x, pv.x, rf.x), fma(beta.y, pv.y, rf.y));
                         sr[slotE + j * nx] = pf[j];
                         if (own[j] && ownf) pP[j * nx] = pf[j];
                     }
@@ -864,8 +859,21 @@ static void launch_pass_ns(const PassArgs& a, int nb, cudaStream_t s) {
     // mu rides in the bulk-copy group when every copy is 16-byte sized and aligned
     const bool mut = (a.op.nx % 2 == 0);
     const bool zc = a.nzch > 1 || a.nzch_tot > 1;
-    auto k = mut ? (zc ? cg_pass_kernel<MAXT, NS, true, RPT, true> : cg_pass_kernel<MAXT, NS, true, RPT, false>)
-                 : (zc ? cg_pass_kernel<MAXT, NS, false, RPT, true> : cg_pass_kernel<MAXT, NS, false, RPT, false>);
+    using KF = void (*)(const PassArgs);
+    KF k = mut ? (zc ? cg_pass_kernel<MAXT, NS, true, RPT, true, 0, 0> : cg_pass_kernel<MAXT, NS, true, RPT, false, 0, 0>)
+               : (zc ? cg_pass_kernel<MAXT, NS, false, RPT, true, 0, 0>
+                     : cg_pass_kernel<MAXT, NS, false, RPT, false, 0, 0>);
+    // compile-time geometries of the BASELINE grids (default ring depth, 2 rows per thread)
+    if (NS == 4 && RPT == 2 && mut && !std::getenv("DOT_CG_GENERIC")) {
+#define DOT_GEOM(GX, GT)                                                                         \
+    if (a.op.nx == GX && a.tl.TY == GT)                                                          \
+        k = zc ? cg_pass_kernel<MAXT, NS, true, RPT, true, GX, GT> : cg_pass_kernel<MAXT, NS, true, RPT, false, GX, GT>;
+        DOT_GEOM(32, 16)
+        DOT_GEOM(64, 11)
+        DOT_GEOM(96, 6)
+        DOT_GEOM(128, 4)
+#undef DOT_GEOM
+    }
     ensure_smem(k, a.tl.smem);
     dim3 grid(a.tl.ntiles * a.nzch, nb);
     k<<<grid, a.tl.threads, a.tl.smem, s>>>(a);
