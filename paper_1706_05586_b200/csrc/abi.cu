@@ -295,6 +295,7 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, c
 
         PassArgs a;
         a.op = P->op;
+        set_edge_coefs(a);
         a.tl = P->tl;
         a.max_iter = P->max_iter;
         a.tol2 = P->tol * P->tol;
@@ -849,6 +850,7 @@ void dd_solve(dot_dd* G, const std::vector<Req>& reqs) {
         }
         PassArgs& a = b.a;
         a.op = P->op;
+        set_edge_coefs(a);
         a.tl = P->tl;
         a.max_iter = P->max_iter;
         a.tol2 = P->tol * P->tol;

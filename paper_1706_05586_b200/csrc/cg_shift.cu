@@ -80,6 +80,16 @@ __host__ __device__ __forceinline__ PlaneCoef plane_coef(const OpConst& op, int 
     return c;
 }
 
+// coefficients of the planes 0, 1, nz-2, nz-1 (precomputed on the host, PassArgs::ec)
+__device__ __forceinline__ PlaneCoef edge_coef(const PassArgs& a, int k) {
+    const int i = k == 0 ? 0 : (k == 1 ? 1 : (k == a.op.nz - 1 ? 3 : 2));
+    PlaneCoef c;
+    c.d = a.ec[i][0];
+    c.wd = a.ec[i][1];
+    c.wu = a.ec[i][2];
+    return c;
+}
+
 // the two real seeds of a pair, componentwise
 __device__ __forceinline__ double2 kt_edge(const PlaneCoef& c, const OpConst& op, double mu, double2 u0, double2 sx,
                                            double2 sy, double2 zd, double2 zu) {
@@ -445,7 +455,7 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
             const double2* sp = sr + slotE;
             if (any2) {
                 const bool interior = g > 1 && g < nz - 2;
-                const PlaneCoef ce = interior ? PlaneCoef{} : plane_coef(a.op, g);
+                const PlaneCoef ce = interior ? PlaneCoef{} : edge_coef(a, g);
                 const double2 alpha = sh_sc.alpha;
                 auto p2 = [&](auto ALL) {
                     constexpr bool A = decltype(ALL)::v != 0;
@@ -453,8 +463,9 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
                     for (int j = 0; j < RPT; ++j) {
                         if (!A && !ph2[j]) continue;
                         const int oj = o + j * nx;
-                        const double2 xw = hasW ? sp[oj - 1] : z2;
-                        const double2 xe = hasE ? sp[oj + 1] : z2;
+                        const double2 vw = sp[oj - 1], ve = sp[oj + 1];   // unconditional: selects, not branches
+                        const double2 xw = hasW ? vw : z2;
+                        const double2 xe = hasE ? ve : z2;
                         const double2 ys = j > 0 ? Pq[j > 0 ? j - 1 : 0][i1] : sp[oj - nx];
                         const double2 yn = j < RPT - 1 ? Pq[j < RPT - 1 ? j + 1 : 0][i1] : sp[oj + nx];
                         mug[j] = MUT ? reinterpret_cast<const double*>(sr + 2 * slotE)[oj] : MU[j][i1];
@@ -493,12 +504,13 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
         if (any_own && tt >= z0 && tt < z1) {
             const double2* rc = rbuf + i2 * rbE + o3;
             const bool interior = tt > 1 && tt < nz - 2;
-            const PlaneCoef ce = interior ? PlaneCoef{} : plane_coef(a.op, tt);
+            const PlaneCoef ce = interior ? PlaneCoef{} : edge_coef(a, tt);
 #pragma unroll
             for (int j = 0; j < RPT; ++j) {
                 if (!own[j]) continue;
-                const double2 xw = hasW ? rc[j * nx - 1] : z2;
-                const double2 xe = hasE ? rc[j * nx + 1] : z2;
+                const double2 vw = rc[j * nx - 1], ve = rc[j * nx + 1];
+                const double2 xw = hasW ? vw : z2;
+                const double2 xe = hasE ? ve : z2;
                 // y-neighbours: own-strip rows from registers (r_{k+1} of plane tt is RN[.][i2])
                 const double2 ys = j > 0 ? RN[j > 0 ? j - 1 : 0][i2] : rc[(j - 1) * nx];
                 const double2 yn = j < RPT - 1 ? RN[j < RPT - 1 ? j + 1 : 0][i2] : rc[(j + 1) * nx];
@@ -887,6 +899,16 @@ static void launch_pass_r(const PassArgs& a, int nb, cudaStream_t s) {
         case 4: launch_pass_ns<MAXT, 4, RPT>(a, nb, s); break;
         case 5: launch_pass_ns<MAXT, 5, RPT>(a, nb, s); break;
         default: throw Error(DOT_ERR_ARG, "pass supports 3..5 ring slots");
+    }
+}
+
+void set_edge_coefs(PassArgs& a) {
+    const int kk[4] = {0, std::min(1, a.op.nz - 1), std::max(a.op.nz - 2, 0), a.op.nz - 1};
+    for (int i = 0; i < 4; ++i) {
+        const PlaneCoef c = plane_coef(a.op, kk[i]);
+        a.ec[i][0] = c.d;
+        a.ec[i][1] = c.wd;
+        a.ec[i][2] = c.wu;
     }
 }
 

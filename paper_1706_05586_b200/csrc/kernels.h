@@ -32,6 +32,7 @@ struct PassArgs {
     double tol2 = 0;              // tol^2
     int nshift = 0;               // frequencies (shifts i omega_f / nu of the scaled system)
     double sigma[kMaxShift] = {}; // omega_f / nu
+    double ec[4][3] = {};         // K~ coefficients (diagonal, down, up) of planes 0, 1, nz-2, nz-1
     const double* mu = nullptr;   // [N] absorption
     double2* R[2] = {nullptr, nullptr};   // [npairs][N] residual r~ of two real seeds (ping-pong)
     double2* Pv[2] = {nullptr, nullptr};  // [npairs][N] direction p~ (ping-pong)
@@ -61,6 +62,8 @@ struct FoldArgs {
     double2* Xs = nullptr;                // [2 npairs][nsl][nP] shifted solutions (scaled variables)
 };
 
+// fills PassArgs::ec from PassArgs::op (call after setting op)
+void set_edge_coefs(PassArgs& a);
 void launch_cg_pass(const PassArgs& a, int nb, cudaStream_t s);
 // zc_own: the z-chunk slot that carries the initial sums (0)
 void launch_cg_init(const PassArgs& a, int nb, cudaStream_t s, int zc_own = 0);
