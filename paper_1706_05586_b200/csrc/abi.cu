@@ -240,9 +240,12 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, c
         if (e) {
             n = std::min(std::max(1, std::atoi(e)), std::max(1, P->nz / 4));
         } else {
-            const long long target = 4LL * P->num_sms;
+            // measured (tools/pass_bench.py, round 2): opt96 at 12 pairs 0.41 / 0.51 / 0.47 of the HBM
+            // peak with 1 / 2 / 4 chunks; sketch32 at 8 pairs 0.06 / 0.09 / 0.13 -- two waves of CTAs,
+            // chunks of >= 8 planes
+            const long long target = 2LL * P->num_sms;
             const long long have = (long long)P->tl.ntiles * nb;
-            if (have < target && P->nz >= 64) n = (int)((target + have - 1) / have);
+            if (have < target && P->nz >= 32) n = (int)((target + have - 1) / have);
             n = std::min(n, std::max(1, P->nz / 8));
         }
         const int zlen = (P->nz + n - 1) / n;

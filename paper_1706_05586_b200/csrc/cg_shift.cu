@@ -876,7 +876,7 @@ static void launch_pass_ns(const PassArgs& a, int nb, cudaStream_t s) {
                : (zc ? cg_pass_kernel<MAXT, NS, false, RPT, true, 0, 0>
                      : cg_pass_kernel<MAXT, NS, false, RPT, false, 0, 0>);
     // compile-time geometries of the BASELINE grids (default ring depth, 2 rows per thread)
-    if (NS == 4 && RPT == 2 && mut && !std::getenv("DOT_CG_GENERIC")) {
+    if constexpr (NS == 4 && RPT == 2) if (mut && !std::getenv("DOT_CG_GENERIC")) {
 #define DOT_GEOM(GX, GT)                                                                         \
     if (a.op.nx == GX && a.tl.TY == GT)                                                          \
         k = zc ? cg_pass_kernel<MAXT, NS, true, RPT, true, GX, GT> : cg_pass_kernel<MAXT, NS, true, RPT, false, GX, GT>;

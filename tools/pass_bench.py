@@ -1,10 +1,10 @@
-"""Quick COCG-pass throughput probe on one bench workload's grid (tiling A/B, not a bench line).
+"""Quick CG-pass throughput probe on one bench workload's grid (tiling A/B, not a bench line).
 
   python tools/pass_bench.py CONFIG NCOLS [REPS]
 Solves NCOLS Rademacher source combinations at every frequency of CONFIG (sampled
-solutions only) REPS times and prints the pass kernel's HBM GB/s (library stats,
-64 B/point/iteration) and its fraction of MEASURED_PEAKS.json.  The tiling knobs
-(DOT_COCG_ZOPT, DOT_COCG_NTX, DOT_COCG_TY, ...) are read from the environment."""
+solutions only) REPS times and prints the pass kernel HBM GB/s (library stats,
+32 B/point/iteration per real seed) and its fraction of MEASURED_PEAKS.json.  The tiling knobs
+(DOT_CG_TY, DOT_CG_ROWS, DOT_CG_ZCHUNKS, ...) are read from the environment."""
 import json
 import os
 import sys
