@@ -58,6 +58,8 @@ struct dot_problem {
     DBuf<int32_t> d_S, d_P, d_S_slot, d_det_slot, d_src_slot, d_off;
     DBuf<double> d_G;
     DBuf<int32_t> d_seg, d_segoff;    // block sparsity of G by basis (GSparse)
+    DBuf<int32_t> d_segslot;          // [T] sample slot of the basis-ordered support points
+    DBuf<double> d_Gseg;              // [T][5] basis-ordered weights
     GSparse gsp;
     DBuf<double2> d_Dt;               // data, [n_freq][n_src][n_det]
     FieldCache cache[2];              // 0: sources, 1: detectors
@@ -1262,6 +1264,8 @@ int dot_set_params(dot_problem* P, const double* p, int where) {
     P->d_G = DBuf<double>(P->arena, std::max<size_t>((size_t)P->K * P->n_p, 1));
     P->d_seg.reset();
     P->d_segoff.reset();
+    P->d_segslot.reset();
+    P->d_Gseg.reset();
     P->gsp = GSparse{};
     launch_compact(P->d_flagS.get(), P->d_posS.get(), N, P->d_S.get(), s);
     launch_compact(P->d_flagP.get(), P->d_posP.get(), N, P->d_P.get(), s);
@@ -1286,6 +1290,11 @@ int dot_set_params(dot_problem* P, const double* p, int where) {
             P->stats.kernel_launches += 5;
             sync(P);
             P->gsp = GSparse{P->d_seg.get(), P->d_segoff.get(), P->n_rbf, T};
+            P->d_segslot = DBuf<int32_t>(P->arena, std::max(T, 1));
+            P->d_Gseg = DBuf<double>(P->arena, 5 * (size_t)std::max(T, 1));
+            launch_compose_index(P->d_seg.get(), T, P->d_S_slot.get(), P->d_segslot.get(), s);
+            launch_seg_weights(P->d_G.get(), P->n_p, P->gsp, P->d_Gseg.get(), s);
+            P->stats.kernel_launches += 2;
         }
     }
     launch_sample_offsets(P->d_P.get(), P->nP, P->nx, P->ny, P->nz, P->tl.TY, P->tl.ntiles, P->d_off.get(), s);
@@ -1363,17 +1372,25 @@ int dot_jacobian(dot_problem* P, const double* W, int32_t ls, const double* V, i
         Jtmp = DBuf<double2>(P->arena, std::max<size_t>(nJ, 1));
         J = Jtmp.get();
     }
-    DBuf<double2> US(P->arena, std::max<size_t>((size_t)nf * ls * K, 1)), LS(P->arena, std::max<size_t>((size_t)nf * ld * K, 1));
-    launch_gather_cols(nf, ls, K, XU, (size_t)ls * P->nP, P->nP, P->d_S_slot.get(), US.get(), (size_t)ls * K, K, s);
-    launch_gather_cols(nf, ld, K, XL, (size_t)ld * P->nP, P->nP, P->d_S_slot.get(), LS.get(), (size_t)ld * K, K, s);
+    // large panels: support fields gathered in basis order (contiguous k per basis); else S order
+    const bool seg = contract_seg_applies(ld, ls, &P->gsp, P->n_p);
+    const int Kp = seg ? (int)P->gsp.total : K;
+    const int32_t* gidx = seg ? P->d_segslot.get() : P->d_S_slot.get();
+    DBuf<double2> US(P->arena, std::max<size_t>((size_t)nf * ls * Kp, 1)), LS(P->arena, std::max<size_t>((size_t)nf * ld * Kp, 1));
+    launch_gather_cols(nf, ls, Kp, XU, (size_t)ls * P->nP, P->nP, gidx, US.get(), (size_t)ls * Kp, Kp, s);
+    launch_gather_cols(nf, ld, Kp, XL, (size_t)ld * P->nP, P->nP, gidx, LS.get(), (size_t)ld * Kp, Kp, s);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (P->timing) {
         e0 = event_at(P, 0);
         e1 = event_at(P, 1);
         DOT_CUDA_TRY(cudaEventRecord(e0, s));
     }
-    launch_contract(nf, K, ld, ls, P->n_p, LS.get(), (size_t)ld * K, US.get(), (size_t)ls * K, P->d_G.get(), J, s,
-                    &P->gsp);
+    if (seg)
+        launch_contract_seg(nf, Kp, ld, ls, P->n_p, P->n_rbf, LS.get(), (size_t)ld * Kp, US.get(), (size_t)ls * Kp,
+                            P->d_Gseg.get(), P->gsp.segoff, J, s);
+    else
+        launch_contract(nf, K, ld, ls, P->n_p, LS.get(), (size_t)ld * K, US.get(), (size_t)ls * K, P->d_G.get(), J, s,
+                        &P->gsp);
     P->stats.kernel_launches += 3;
     if (P->timing) {
         DOT_CUDA_TRY(cudaEventRecord(e1, s));
@@ -1760,10 +1777,23 @@ int dot_contract_fields(dot_problem* P, int32_t ld, int32_t ls, const double* La
         e1 = event_at(P, 1);
         DOT_CUDA_TRY(cudaEventRecord(e0, s));
     }
-    launch_contract(nf, K, ld, ls, P->n_p, reinterpret_cast<const double2*>(Lam), (size_t)ld * K,
-                    reinterpret_cast<const double2*>(U), (size_t)ls * K, P->d_G.get(), reinterpret_cast<double2*>(J), s,
-                    &P->gsp);
-    P->stats.kernel_launches++;
+    if (contract_seg_applies(ld, ls, &P->gsp, P->n_p)) {
+        // reorder the S-ordered panels into basis order (one gather), then the segment GEMM
+        const int T = (int)P->gsp.total;
+        DBuf<double2> Lg(P->arena, std::max<size_t>((size_t)nf * ld * T, 1)), Ug(P->arena, std::max<size_t>((size_t)nf * ls * T, 1));
+        launch_gather_cols(nf, ld, T, reinterpret_cast<const double2*>(Lam), (size_t)ld * K, K, P->gsp.seg, Lg.get(),
+                           (size_t)ld * T, T, s);
+        launch_gather_cols(nf, ls, T, reinterpret_cast<const double2*>(U), (size_t)ls * K, K, P->gsp.seg, Ug.get(),
+                           (size_t)ls * T, T, s);
+        launch_contract_seg(nf, T, ld, ls, P->n_p, P->n_rbf, Lg.get(), (size_t)ld * T, Ug.get(), (size_t)ls * T,
+                            P->d_Gseg.get(), P->gsp.segoff, reinterpret_cast<double2*>(J), s);
+        P->stats.kernel_launches += 3;
+    } else {
+        launch_contract(nf, K, ld, ls, P->n_p, reinterpret_cast<const double2*>(Lam), (size_t)ld * K,
+                        reinterpret_cast<const double2*>(U), (size_t)ls * K, P->d_G.get(), reinterpret_cast<double2*>(J),
+                        s, &P->gsp);
+        P->stats.kernel_launches++;
+    }
     if (P->timing) {
         DOT_CUDA_TRY(cudaEventRecord(e1, s));
         DOT_CUDA_TRY(cudaEventSynchronize(e1));

@@ -388,6 +388,159 @@ __global__ void __launch_bounds__(THREADS) contract_gemm_sparse_kernel(
     }
 }
 
+// ------------------------------------- block-sparse GEMM on basis-ordered panels (default)
+// The support fields are gathered once per call in BASIS order: panel column t of basis j
+// (segoff[j] <= t < segoff[j+1]) is support point seg[t] (only the nonzero
+// components of dA/dp_k enter).  Per (frequency, basis) one complex GEMM with CONTIGUOUS k:
+//     J[d][(q, i)] = - sum_{t in basis j} Lam[d][t] * (Gs[t][q] U[i][t]),   q < 5,
+// M = ld, N = 5 ls.  Tiles 64 x 64, k-tiles of 16, a 3-stage cp.async pipeline (16-byte
+// copies, zero fill past the panel), and the 3-multiply complex product
+//     P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi);  re = P1 - P2, im = P3 - P1 - P2
+// (3 DMMA per fragment instead of 4).  B = Gs * U is formed in the fragment load.
+// Warp w: rows 16 (w & 3) .. +16, columns 32 (w >> 2) .. +32.
+constexpr int QM = 64, QN = 64, QK = 16, QRS = QK + 1, QST = 3;   // QRS: padded row stride (double2)
+constexpr size_t kSegStage = (size_t)(QM + QN) * QRS * sizeof(double2) + QK * 5 * sizeof(double);
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1) contract_seg_kernel(int T, int ld, int ls, int n_rbf,
+                                                                 const double2* __restrict__ Lam, size_t lam_bs,
+                                                                 const double2* __restrict__ U, size_t u_bs,
+                                                                 const double* __restrict__ Gs,
+                                                                 const int32_t* __restrict__ segoff, int n_p,
+                                                                 double2* J) {
+    extern __shared__ __align__(16) unsigned char qsm[];
+    auto stA = [&](int st) { return reinterpret_cast<double2*>(qsm + st * kSegStage); };
+    auto stU = [&](int st) { return stA(st) + QM * QRS; };
+    auto stG = [&](int st) { return reinterpret_cast<double*>(stU(st) + QN * QRS); };
+    const int f = blockIdx.z / n_rbf, jb = blockIdx.z % n_rbf;
+    const int d0 = blockIdx.x * QM, n0 = blockIdx.y * QN;
+    const int N5 = 5 * ls;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;
+    const double2* Lf = Lam + (size_t)f * lam_bs;
+    const double2* Uf = U + (size_t)f * u_bs;
+    const int s0 = segoff[jb], s1 = segoff[jb + 1];
+    const int nkt = (s1 - s0 + QK - 1) / QK;
+    // loader: 4 A and 4 U elements per thread per k-tile (row = idx / 16, kk = idx % 16)
+    const double2* asrc[4];
+    const double2* usrc[4];
+    bool aok[4], uok[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int idx = threadIdx.x + e * THREADS, row = idx / QK;
+        const int d = d0 + row, n = n0 + row;
+        aok[e] = d < ld;
+        uok[e] = n < N5;
+        const int q = uok[e] ? n / ls : 0, i = uok[e] ? n - q * ls : 0;
+        asrc[e] = Lf + (size_t)(aok[e] ? d : 0) * T + s0 + (idx % QK);
+        usrc[e] = Uf + (size_t)i * T + s0 + (idx % QK);
+    }
+    auto load = [&](int kt, int st) {          // k-tile kt (0-based within the basis) -> stage st
+        const int k0 = kt * QK;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int idx = threadIdx.x + e * THREADS, row = idx / QK, kk = idx % QK;
+            const bool kin = s0 + k0 + kk < s1;
+            cp_async16(stA(st) + row * QRS + kk, kin && aok[e] ? asrc[e] + k0 : Lf, kin && aok[e]);
+            cp_async16(stU(st) + row * QRS + kk, kin && uok[e] ? usrc[e] + k0 : Uf, kin && uok[e]);
+        }
+        if (threadIdx.x < QK * 5) {
+            const int kk = threadIdx.x / 5, q = threadIdx.x % 5;
+            const int t = s0 + k0 + kk;
+            stG(st)[kk * 5 + q] = t < s1 ? Gs[(size_t)t * 5 + q] : 0.0;
+        }
+    };
+    // per-thread fragment columns: n = wn + ni*8 + lane/4 -> parameter q of that column
+    int qn[4];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+        const int n = n0 + wn + ni * 8 + (lane >> 2);
+        qn[ni] = n < N5 ? n / ls : 0;
+    }
+    double p1[2][4][2], p2[2][4][2], p3[2][4][2];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) p1[mi][ni][h] = p2[mi][ni][h] = p3[mi][ni][h] = 0.0;
+#pragma unroll
+    for (int st = 0; st < QST - 1; ++st) {
+        if (st < nkt) load(st, st);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int kt = 0; kt < nkt; ++kt) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(QST - 2) : "memory");
+        __syncthreads();                       // stage kt landed (and the G tile stores)
+        const int st = kt % QST;
+        if (kt + QST - 1 < nkt) load(kt + QST - 1, (kt + QST - 1) % QST);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        const double2* A = stA(st);
+        const double2* Ub = stU(st);
+        const double* Gt = stG(st);
+#pragma unroll
+        for (int k4 = 0; k4 < QK; k4 += 4) {
+            const int kk = k4 + (lane & 3);
+            double ar[2], ai[2], as[2];
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi) {
+                const double2 a = A[(wm + mi * 8 + (lane >> 2)) * QRS + kk];
+                ar[mi] = a.x;
+                ai[mi] = a.y;
+                as[mi] = a.x + a.y;
+            }
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+                const double2 u = Ub[(wn + ni * 8 + (lane >> 2)) * QRS + kk];
+                const double g = Gt[kk * 5 + qn[ni]];
+                const double br = g * u.x, bi = g * u.y, bs = br + bi;
+#pragma unroll
+                for (int mi = 0; mi < 2; ++mi) {
+                    dmma(p1[mi][ni][0], p1[mi][ni][1], ar[mi], br);
+                    dmma(p2[mi][ni][0], p2[mi][ni][1], ai[mi], bi);
+                    dmma(p3[mi][ni][0], p3[mi][ni][1], as[mi], bs);
+                }
+            }
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    // epilogue: J[f][(d, i)][5 jb + q] = -C[d][(q, i)]
+    const int npairs = ld * ls;
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+        const int d = d0 + wm + mi * 8 + (lane >> 2);
+        if (d >= ld) continue;
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int n = n0 + wn + ni * 8 + 2 * (lane & 3) + h;
+                if (n >= N5) continue;
+                const int q = n / ls, i = n - q * ls;
+                const double re = p1[mi][ni][h] - p2[mi][ni][h];
+                const double im = p3[mi][ni][h] - p1[mi][ni][h] - p2[mi][ni][h];
+                J[((size_t)f * npairs + (size_t)d * ls + i) * n_p + 5 * jb + q] = make_double2(-re, -im);
+            }
+    }
+}
+
+// Gs[t][q] = G[seg[t]][5 j + q] for the points t of basis j (basis-ordered weights)
+__global__ void seg_weights_kernel(const double* __restrict__ G, int n_p, const int32_t* seg, const int32_t* segoff,
+                                   double* Gs) {
+    const int j = blockIdx.y;
+    for (int t = segoff[j] + blockIdx.x * blockDim.x + threadIdx.x; t < segoff[j + 1]; t += gridDim.x * blockDim.x)
+        for (int q = 0; q < 5; ++q) Gs[(size_t)t * 5 + q] = 5 * j + q < n_p ? G[(size_t)seg[t] * n_p + 5 * j + q] : 0.0;
+}
+
+// idx[t] = slot[seg[t]]
+__global__ void compose_index_kernel(const int32_t* seg, int T, const int32_t* slot, int32_t* idx) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) idx[t] = slot[seg[t]];
+}
+
 __global__ void rbf_flags_kernel(const double* __restrict__ G, int K, int n_p, int n_rbf, int32_t* F) {
     const size_t tot = (size_t)K * n_rbf;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
@@ -422,6 +575,38 @@ void launch_rbf_segments(const int32_t* F, const int32_t* pos, int K, int n_rbf,
     const size_t tot = (size_t)K * n_rbf;
     rbf_segments_kernel<<<(unsigned)std::max<size_t>(1, std::min<size_t>((tot + 255) / 256, 8192)), 256, 0, s>>>(
         F, pos, K, n_rbf, total, seg, off);
+    DOT_CUDA_TRY(cudaGetLastError());
+}
+
+bool contract_seg_applies(int ld, int ls, const GSparse* sp, int n_p) {
+    return sp && sp->seg && sp->n_rbf * 5 == n_p && ld >= 32 && ls >= 8 && !std::getenv("DOT_CONTRACT_OLD");
+}
+
+void launch_contract_seg(int nb, int T, int ld, int ls, int n_p, int n_rbf, const double2* Lam, size_t lam_bstride,
+                         const double2* U, size_t u_bstride, const double* Gs, const int32_t* segoff, double2* J,
+                         cudaStream_t s) {
+    if (nb <= 0 || ld <= 0 || ls <= 0) return;
+    if (T <= 0) {
+        DOT_CUDA_TRY(cudaMemsetAsync(J, 0, (size_t)nb * ld * ls * n_p * sizeof(double2), s));
+        return;
+    }
+    dim3 grid((ld + QM - 1) / QM, (5 * ls + QN - 1) / QN, n_rbf * nb);
+    const size_t smem = QST * kSegStage;
+    ensure_smem(contract_seg_kernel, smem);
+    contract_seg_kernel<<<grid, THREADS, smem, s>>>(T, ld, ls, n_rbf, Lam, lam_bstride, U, u_bstride, Gs, segoff,
+                                                      n_p, J);
+    DOT_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_seg_weights(const double* G, int n_p, const GSparse& sp, double* Gs, cudaStream_t s) {
+    if (sp.total <= 0) return;
+    seg_weights_kernel<<<dim3(32, sp.n_rbf), 256, 0, s>>>(G, n_p, sp.seg, sp.segoff, Gs);
+    DOT_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_compose_index(const int32_t* seg, int T, const int32_t* slot, int32_t* idx, cudaStream_t s) {
+    if (T <= 0) return;
+    compose_index_kernel<<<(unsigned)std::min(1024, (T + 255) / 256), 256, 0, s>>>(seg, T, slot, idx);
     DOT_CUDA_TRY(cudaGetLastError());
 }
 

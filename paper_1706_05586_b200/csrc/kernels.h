@@ -126,6 +126,17 @@ struct GSparse {
 void launch_contract(int nb, int K, int ld, int ls, int n_p, const double2* Lam, size_t lam_bstride,
                      const double2* U, size_t u_bstride, const double* G, double2* J,
                      cudaStream_t s, const GSparse* sp = nullptr);
+// Block-sparse GEMM on basis-ordered panels (the default for large panels): Lam [nb][ld][T],
+// U [nb][ls][T] with column t the support point seg[t] of basis j (segoff[j] <= t < segoff[j+1]),
+// Gs [T][5] the basis's weights there.  contract_seg_applies: the panel shape takes this path.
+bool contract_seg_applies(int ld, int ls, const GSparse* sp, int n_p);
+void launch_contract_seg(int nb, int T, int ld, int ls, int n_p, int n_rbf, const double2* Lam, size_t lam_bstride,
+                         const double2* U, size_t u_bstride, const double* Gs, const int32_t* segoff, double2* J,
+                         cudaStream_t s);
+// Gs[t][q] = G[seg[t]][5 j + q]
+void launch_seg_weights(const double* G, int n_p, const GSparse& sp, double* Gs, cudaStream_t s);
+// idx[t] = slot[seg[t]]
+void launch_compose_index(const int32_t* seg, int T, const int32_t* slot, int32_t* idx, cudaStream_t s);
 // flags F[j][s] = any(G[s][5j .. 5j+4] != 0), j < n_rbf
 void launch_rbf_flags(const double* G, int K, int n_rbf, int32_t* F, cudaStream_t s);
 // out[pos[i]] = i % K for flagged i (segment lists), off[j] = pos[j*K], off[n_rbf] = *total
