@@ -410,9 +410,9 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
             for (int j = 0; j < RPT; ++j)
                 if (ph2[j]) MU[j][i0] = pMu[(size_t)f * PS + j * nx];
         // ---- phase 1: plane f
+        // (zeros are assigned only on the paths that need them: rows outside the domain, and
+        // the tail steps past the last plane -- no per-step register clears)
         double2 pf[RPT];
-#pragma unroll
-        for (int j = 0; j < RPT; ++j) pf[j] = z2;
         if (f < b1) {
             asm volatile(
                 "{\n\t.reg .pred p;\n\t"
@@ -428,7 +428,10 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
                     constexpr bool A = decltype(ALL)::v != 0;
 #pragma unroll
                     for (int j = 0; j < RPT; ++j) {
-                        if (!A && !indom[j]) continue;
+                        if (!A && !indom[j]) {
+                            pf[j] = z2;
+                            continue;
+                        }
                         const double2 rf = sr[j * nx];
                         const double2 pv = sr[slotE + j * nx];
                         pf[j] = cmk(fma(beta.x, pv.x, rf.x), fma(beta.y, pv.y, rf.y));
@@ -438,16 +441,17 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
                 };
                 if (all_in) p1(IC<1>());
                 else p1(IC<0>());
+            } else {
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) pf[j] = z2;
             }
+        } else {
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) pf[j] = z2;
         }
         // ---- phase 2: plane g = f - 1
         double2 rng[RPT];
-        double mug[RPT];
-#pragma unroll
-        for (int j = 0; j < RPT; ++j) {
-            rng[j] = z2;
-            mug[j] = 0.0;
-        }
+        double mug[RPT];           // read (phase 3 via mu_carry) only for rows that assign it
         const int g = f - 1;
         if (g >= a2 && g < b2) {
             const bool owng = !ZC || (g >= z0 && g < z1);
@@ -461,7 +465,10 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
                     constexpr bool A = decltype(ALL)::v != 0;
 #pragma unroll
                     for (int j = 0; j < RPT; ++j) {
-                        if (!A && !ph2[j]) continue;
+                        if (!A && !ph2[j]) {
+                            rng[j] = z2;
+                            continue;
+                        }
                         const int oj = o + j * nx;
                         const double2 vw = sp[oj - 1], ve = sp[oj + 1];   // unconditional: selects, not branches
                         const double2 xw = hasW ? vw : z2;
@@ -488,6 +495,9 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
                 };
                 if (all2) p2(IC<1>());
                 else p2(IC<0>());
+            } else {
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) rng[j] = z2;
             }
             if (a.nP > 0 && owng) {        // r_k at the samples of plane g (history for the fold)
                 const int2 sr2 = s_samp[g];
@@ -496,6 +506,9 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
                     Hk[si] = sr[rem - (j0 - 2) * nx];
                 }
             }
+        } else {
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) rng[j] = z2;
         }
 #pragma unroll
         for (int j = 0; j < RPT; ++j) Pq[j][i0] = pf[j];
