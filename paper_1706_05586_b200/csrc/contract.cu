@@ -264,130 +264,6 @@ __global__ void __launch_bounds__(THREADS) contract_sparse_kernel(int K, int ld,
     }
 }
 
-// ------------------------------------------------- block-sparse, GEMM formulation
-// Per (frequency, basis j) the 5 parameter columns are ONE complex GEMM over the
-// basis's support points S_j:
-//     J[d][(q, i)] = - sum_{s in S_j} Lam[d][s] * (G[s][5j+q] U[i][s]),   q < 5,
-// M = ld, N = 5 ls, K = |S_j|, complex x complex (4 real DMMA products per
-// fragment: re = Ar Br - Ai Bi, im = Ar Bi + Ai Br).  Tiles 64 (d) x 64 (q,i),
-// k-tiles of 16 support points gathered through the segment list, double-
-// buffered in shared memory.  Warp w: rows 16 (w & 3) .. +16, columns 32 (w >> 2) .. +32.
-constexpr int GTM = 64, GTN = 64, GBK = 16, GKS = GBK + 4;
-
-__global__ void __launch_bounds__(THREADS) contract_gemm_sparse_kernel(
-    int K, int ld, int ls, int n_p, int n_rbf, const double2* __restrict__ Lam, size_t lam_bs,
-    const double2* __restrict__ U, size_t u_bs, const double* __restrict__ G, const int32_t* __restrict__ seg,
-    const int32_t* __restrict__ segoff, double2* J) {
-    extern __shared__ __align__(16) double gsm[];
-    // [2 bufs][re/im][GTM rows][GKS] for A, then the same for B
-    auto Ab = [&](int bb, int c) { return gsm + ((bb * 2 + c) * GTM) * GKS; };
-    auto Bb = [&](int bb, int c) { return gsm + 4 * GTM * GKS + ((bb * 2 + c) * GTN) * GKS; };
-    const int f = blockIdx.z / n_rbf, jb = blockIdx.z % n_rbf;
-    const int d0 = blockIdx.x * GTM, n0 = blockIdx.y * GTN;     // n = q * ls + i
-    const int N5 = 5 * ls;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;
-    const double2* Lf = Lam + (size_t)f * lam_bs;
-    const double2* Uf = U + (size_t)f * u_bs;
-    const int s0 = segoff[jb], s1 = segoff[jb + 1];
-    // loader mapping: each thread moves 4 A and 4 B elements per k-tile (64 x 16 each)
-    constexpr int EPT = GTM * GBK / THREADS;   // 4
-    double2 av[EPT], bv[EPT];
-    auto load = [&](int kt) {
-#pragma unroll
-        for (int e = 0; e < EPT; ++e) {
-            const int idx = threadIdx.x + e * THREADS;
-            const int row = idx / GBK, kk = idx % GBK;
-            const int t = kt + kk;
-            const bool okk = t < s1;
-            const int node = okk ? seg[t] : 0;
-            const int d = d0 + row;
-            av[e] = (okk && d < ld) ? Lf[(size_t)d * K + node] : make_double2(0.0, 0.0);
-            const int n = n0 + row;
-            if (okk && n < N5) {
-                const int q = n / ls, i = n - q * ls;
-                const double g = G[(size_t)node * n_p + 5 * jb + q];
-                const double2 u = Uf[(size_t)i * K + node];
-                bv[e] = make_double2(g * u.x, g * u.y);
-            } else {
-                bv[e] = make_double2(0.0, 0.0);
-            }
-        }
-    };
-    auto store = [&](int bb) {
-#pragma unroll
-        for (int e = 0; e < EPT; ++e) {
-            const int idx = threadIdx.x + e * THREADS;
-            const int row = idx / GBK, kk = idx % GBK;
-            Ab(bb, 0)[row * GKS + kk] = av[e].x;
-            Ab(bb, 1)[row * GKS + kk] = av[e].y;
-            Bb(bb, 0)[row * GKS + kk] = bv[e].x;
-            Bb(bb, 1)[row * GKS + kk] = bv[e].y;
-        }
-    };
-    // accumulators: [mi 2][ni 4] fragments, re and im, 2 doubles each
-    double cr[2][4][2], ci[2][4][2];
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) cr[mi][ni][0] = cr[mi][ni][1] = ci[mi][ni][0] = ci[mi][ni][1] = 0.0;
-    if (s0 < s1) {
-        load(s0);
-        store(0);
-    }
-    __syncthreads();
-    int bb = 0;
-    for (int kt = s0; kt < s1; kt += GBK) {
-        const bool more = kt + GBK < s1;
-        if (more) load(kt + GBK);
-#pragma unroll
-        for (int k4 = 0; k4 < GBK; k4 += 4) {
-            double ar[2], ai[2], brr[4], bii[4];
-#pragma unroll
-            for (int mi = 0; mi < 2; ++mi) {
-                const int r = wm + mi * 8 + (lane >> 2);
-                ar[mi] = Ab(bb, 0)[r * GKS + k4 + (lane & 3)];
-                ai[mi] = Ab(bb, 1)[r * GKS + k4 + (lane & 3)];
-            }
-#pragma unroll
-            for (int ni = 0; ni < 4; ++ni) {
-                const int c = wn + ni * 8 + (lane >> 2);
-                brr[ni] = Bb(bb, 0)[c * GKS + k4 + (lane & 3)];
-                bii[ni] = Bb(bb, 1)[c * GKS + k4 + (lane & 3)];
-            }
-#pragma unroll
-            for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-                for (int ni = 0; ni < 4; ++ni) {
-                    dmma(cr[mi][ni][0], cr[mi][ni][1], ar[mi], brr[ni]);
-                    dmma(cr[mi][ni][0], cr[mi][ni][1], -ai[mi], bii[ni]);
-                    dmma(ci[mi][ni][0], ci[mi][ni][1], ar[mi], bii[ni]);
-                    dmma(ci[mi][ni][0], ci[mi][ni][1], ai[mi], brr[ni]);
-                }
-        }
-        if (more) store(bb ^ 1);
-        __syncthreads();
-        bb ^= 1;
-    }
-    // epilogue: J[f][(d, i)][5 jb + q] = -C[d][(q, i)]
-    const int npairs = ld * ls;
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi) {
-        const int d = d0 + wm + mi * 8 + (lane >> 2);
-        if (d >= ld) continue;
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int n = n0 + wn + ni * 8 + 2 * (lane & 3) + h;
-                if (n >= N5) continue;
-                const int q = n / ls, i = n - q * ls;
-                const size_t pair = (size_t)d * ls + i;
-                J[((size_t)f * npairs + pair) * n_p + 5 * jb + q] = make_double2(-cr[mi][ni][h], -ci[mi][ni][h]);
-            }
-    }
-}
-
 // ------------------------------------- block-sparse GEMM on basis-ordered panels (default)
 // The support fields are gathered once per call in BASIS order: panel column t of basis j
 // (segoff[j] <= t < segoff[j+1]) is support point seg[t] (only the nonzero
@@ -579,7 +455,7 @@ void launch_rbf_segments(const int32_t* F, const int32_t* pos, int K, int n_rbf,
 }
 
 bool contract_seg_applies(int ld, int ls, const GSparse* sp, int n_p) {
-    return sp && sp->seg && sp->n_rbf * 5 == n_p && ld >= 32 && ls >= 8 && !std::getenv("DOT_CONTRACT_OLD");
+    return sp && sp->seg && sp->n_rbf * 5 == n_p && ld >= 32 && ls >= 8;
 }
 
 void launch_contract_seg(int nb, int T, int ld, int ls, int n_p, int n_rbf, const double2* Lam, size_t lam_bstride,
@@ -617,16 +493,6 @@ void launch_contract(int nb, int K, int ld, int ls, int n_p, const double2* Lam,
     if (nb <= 0 || npairs <= 0 || n_p <= 0) return;
     if (K <= 0) {
         DOT_CUDA_TRY(cudaMemsetAsync(J, 0, (size_t)nb * npairs * n_p * sizeof(double2), s));
-        return;
-    }
-    if (sp && sp->seg && sp->n_rbf * 5 == n_p && ld >= 32 && ls >= 8) {
-        // large panels: per (frequency, basis) complex GEMM on the tensor pipe
-        dim3 grid((ld + GTM - 1) / GTM, (5 * ls + GTN - 1) / GTN, sp->n_rbf * nb);
-        const size_t smem = (size_t)8 * GTM * GKS * sizeof(double);
-        ensure_smem(contract_gemm_sparse_kernel, smem);
-        contract_gemm_sparse_kernel<<<grid, THREADS, smem, s>>>(K, ld, ls, n_p, sp->n_rbf, Lam, lam_bstride, U,
-                                                                u_bstride, G, sp->seg, sp->segoff, J);
-        DOT_CUDA_TRY(cudaGetLastError());
         return;
     }
     if (sp && sp->seg && sp->n_rbf * 5 == n_p) {

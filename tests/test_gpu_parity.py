@@ -195,25 +195,34 @@ def test_contract_kernel_against_direct_sums(dot):
 
 
 def test_solve_accounting_reproduces_table4(dot):
-    """PAPER.md Table 4 arithmetic with the library's solve counter: SAA with
-    l = 10 for 10 function and 5 Jacobian evaluations costs 150 solves
-    (forward fields are reused by the Jacobian); one optimized-direction
-    replacement adds n_s + n_d = 64 (32 sources, 32 detectors, one frequency)."""
+    """PAPER.md Table 4 arithmetic (tests/golden/table1_svd_sizes.json "table4_pde_solves",
+    cited there) with the library's solve counter: SAA with l = 10 for F = 10 function and
+    J = 5 Jacobian evaluations costs F*l + J*l = 150 solves (forward fields are reused by the
+    Jacobian); one optimized-direction replacement event adds n_s + n_d = 64 (32 sources,
+    32 detectors, one frequency) -- the "Replacing" rows' full_jacobian_events term."""
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table1_svd_sizes.json")))
+    saa = gold["table4_pde_solves"]["rows"][0]
+    F, Jn, l = saa["F"], saa["J"], saa["l"]
     cfg = small_config(n=(32, 16, 6), L=(8.0, 4.0, 2.0), src=(8, 4), det=(8, 4), freqs=(0.0,), eps=0.4)
     prob, wl = small_problem(cfg)
     g = gpu_problem(dot, cfg, prob, wl)
     g.reset_stats()
     rng = np.random.default_rng(0)
-    W = np.sign(rng.standard_normal((32, 10)))
-    V = np.sign(rng.standard_normal((32, 10)))
-    for it in range(10):
+    W = np.sign(rng.standard_normal((32, l)))
+    V = np.sign(rng.standard_normal((32, l)))
+    for it in range(F):
         g.set_params(wl.p * (1 + 1e-3 * it))
         g.misfit(W, V)
-        if it % 2 == 0:
+        if it % (F // Jn) == 0:
             g.jacobian(W, V)
-    assert g.stats()["rhs_solved"] == 150
+    assert g.stats()["rhs_solved"] == F * l + Jn * l == saa["total"]
     g.optimize_directions(1, W, V)
-    assert g.stats()["rhs_solved"] == 150 + 64
+    # each replacement event costs the full-data solves n_s + n_d (per frequency)
+    for row in gold["table4_pde_solves"]["rows"][1:3]:
+        assert row["total"] == (row["F"] + row["J"]) * row["l"] + row["full_jacobian_events"] * 64
+    assert g.stats()["rhs_solved"] == saa["total"] + 64
 
 
 def test_optimize_directions_parity(dot):
