@@ -268,7 +268,9 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
     double2* slots = reinterpret_cast<double2*>(smem_raw);          // [NS][slotW]
     double2* rbuf = slots + (size_t)NS * slotW;                     // [3][rowsR*nx]
     uint64_t* bars = reinterpret_cast<uint64_t*>(rbuf + 3 * rbE);
-    double* scratch = reinterpret_cast<double*>(bars + NS);         // [32][kNumPartials]
+    // bars[0, NS): TMA ring slots; bars[NS], bars[NS + 1]: step barriers (every thread arrives after
+    // its step, a warp waits for the previous step's arrivals only before reading neighbours' data)
+    double* scratch = reinterpret_cast<double*>(bars + NS + 2);     // [32][kNumPartials]
     int2* s_samp = reinterpret_cast<int2*>(scratch + 32 * kNumPartials);   // [nz] sample ranges
     __shared__ PairScalars sh_sc;
 
@@ -300,6 +302,8 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
     if (threadIdx.x == 0) {
         for (int q = 0; q < NS; ++q)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bars[q])), "r"(1));
+        for (int q = NS; q < NS + 2; ++q)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bars[q])), "r"((int)blockDim.x));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -398,12 +402,13 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
     uint32_t par = 0;                  // mbarrier parity of plane f
     int sl_prev = NS - 1;              // ring slot of plane f - 1
     int sl_iss = PD % NS;              // ring slot of plane f + PD
+    int sidx = 0;                      // step counter (step barrier = bars[NS + (sidx & 1)])
+    const uint32_t sbar0 = bar0 + 8 * NS;
 
     auto step = [&](int f, auto IDX) {
         constexpr int i0 = decltype(IDX)::v;           // f % 3
         constexpr int i1 = (i0 + 2) % 3;               // (f - 1) % 3
         constexpr int i2 = (i0 + 1) % 3;               // (f - 2) % 3
-        if (threadIdx.x == 0 && f + PD < b1) issue(f + PD, sl_iss);
         const bool ownf = !ZC || (f >= z0 && f < z1);
         if (!MUT && f < b1)
 #pragma unroll
@@ -449,6 +454,20 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
 #pragma unroll
             for (int j = 0; j < RPT; ++j) pf[j] = z2;
         }
+        // ---- every thread's step f-1 (smem p of plane f-1, Rbuf of plane f-2, reads of the ring slot
+        // of plane f-2) must be complete before phase 2 reads neighbours and before that slot is
+        // refilled; phase 1 above only touched this thread's own rows of the plane-f slot
+        if (sidx > 0) {
+            const int ps = sidx - 1;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "WAITS_%=:\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                "@!p bra WAITS_%=;\n\t}" ::"r"(sbar0 + 8 * (ps & 1)),
+                "r"((ps >> 1) & 1)
+                : "memory");
+        }
+        if (threadIdx.x == 0 && f + PD < b1) issue(f + PD, sl_iss);
         // ---- phase 2: plane g = f - 1
         double2 rng[RPT];
         double mug[RPT];           // read (phase 3 via mu_carry) only for rows that assign it
@@ -554,7 +573,8 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
             par ^= 1u;
         }
         if (++sl_iss == NS) sl_iss = 0;
-        __syncthreads();
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sbar0 + 8 * (sidx & 1)) : "memory");
+        ++sidx;
     };
     // RN[.][i0] read in phase 3 is r_{k+1}(f-3), written three steps earlier.
 #pragma unroll 1
@@ -836,7 +856,7 @@ __global__ void pack_planes_kernel(const double2* A, const double2* B, size_t N,
 size_t pass_smem(int nx, int TY, int NS, int nz) {
     const size_t slotE = (size_t)(TY + 4) * nx;
     const size_t e = (size_t)NS * (2 * slotE + (nx % 2 == 0 ? (slotE + 1) / 2 : 0)) + 3 * (size_t)(TY + 2) * nx;
-    return e * sizeof(double2) + NS * 8 + 32 * kNumPartials * 8 + 8 * (size_t)nz + 128;
+    return e * sizeof(double2) + (NS + 2) * 8 + 32 * kNumPartials * 8 + 8 * (size_t)nz + 128;
 }
 
 // Pass tiling: a thread owns `rows` slot rows of one column of the TY + 4 slot rows.
