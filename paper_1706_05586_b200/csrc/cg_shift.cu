@@ -531,6 +531,10 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
         }
 #pragma unroll
         for (int j = 0; j < RPT; ++j) Pq[j][i0] = pf[j];
+        // this step's shared-memory writes are done (phase 3 writes only registers and HBM): arrive.
+        // The next step's waits then also cover this thread's phase-3 reads of Rbuf plane f - 2,
+        // which is rewritten two steps later only.
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sbar0 + 8 * (sidx & 1)) : "memory");
         // ---- phase 3: plane tt = f - 2
         const int tt = f - 2;
         if (any_own && tt >= z0 && tt < z1) {
@@ -573,7 +577,6 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
             par ^= 1u;
         }
         if (++sl_iss == NS) sl_iss = 0;
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sbar0 + 8 * (sidx & 1)) : "memory");
         ++sidx;
     };
     // RN[.][i0] read in phase 3 is r_{k+1}(f-3), written three steps earlier.
