@@ -198,3 +198,49 @@ def test_opt96_step_optimized_directions_full_size():
     ref = -np.einsum("jx,xk,ix->jik", y[:, S], Gfull[S], z[:, S])
     got = J2[f][np.ix_(jcol, icol)]
     assert np.linalg.norm(got - ref) <= 1e-7 * np.linalg.norm(ref)
+
+
+def test_all128_jacobian_entries_against_dense_fields():
+    """configs[4] grid (128^3, 5 frequencies, 160 parameters, |S| ~ 6e4): the Jacobian of 8
+    point sources x 32 point detectors (ld >= 32, ls >= 8: the basis-ordered block-sparse
+    GEMM of the all-sources step) against the direct sum over dense fields with the oracle's
+    dA/dp (Eq. (Jacobian kth column), L966-972), 1e-7 relative Frobenius; the dense fields
+    are pinned by their true residual under the oracle operator (Eq. (2.1))."""
+    from paper_1706_05586_b200 import build
+    build.build()
+    import paper_1706_05586_b200 as dot
+    from oracle import assemble
+    cfg = config_by_name("all128")
+    wl = make_workload(cfg)
+    g = dot.DOTProblem.from_config(cfg, wl.src_nodes, wl.det_nodes, max_rhs=200)
+    g.set_params(wl.p)
+    grid = make_grid(cfg.n, cfg.L)
+    src_cols = np.arange(8) * 131 % cfg.n_s
+    det_cols = np.arange(32) * 31 % cfg.n_d
+    Es = np.zeros((cfg.n_s, 8))
+    Es[src_cols, np.arange(8)] = 1.0
+    Ed = np.zeros((cfg.n_d, 32))
+    Ed[det_cols, np.arange(32)] = 1.0
+    J = g.jacobian(Es, Ed)                              # [f][32][8][n_p]
+    assert J.shape == (cfg.n_freq, 32, 8, cfg.n_p)
+    Gfull = jacobian_weights(wl.p, grid, cfg)
+    S = np.nonzero(np.abs(Gfull).sum(1) > 0)[0]
+    mu = absorption(wl.p, grid, cfg)
+    scale = grid.theta[wl.src_nodes] / grid.cell_volume
+    f = 3
+    A = assemble(grid, cfg.D, mu, 2 * np.pi * cfg.freqs_hz[f], cfg.nu).tocsr()
+    si, di = [1, 6], [0, 29]                            # entries checked: 2 sources x 2 detectors
+    b = np.zeros((2, grid.N), complex)
+    c = np.zeros((2, grid.N), complex)
+    for r, k in enumerate(si):
+        b[r, wl.src_nodes[src_cols[k]]] = scale[src_cols[k]]
+    for r, k in enumerate(di):
+        c[r, wl.det_nodes[det_cols[k]]] = 1.0
+    z, _ = g.solve(b, f)
+    y, _ = g.solve(c, f)
+    for rhs, sol in ((b, z), (c, y)):
+        for r in range(2):
+            assert np.linalg.norm(rhs[r] - A @ sol[r]) <= 1e-14 * np.linalg.norm(rhs[r])
+    ref = -np.einsum("jx,xk,ix->jik", y[:, S], Gfull[S], z[:, S])
+    got = J[f][np.ix_(di, si)]
+    assert np.linalg.norm(got - ref) <= 1e-7 * np.linalg.norm(ref)

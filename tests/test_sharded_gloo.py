@@ -72,7 +72,7 @@ CASES = {2: dict(n=(7, 7, 5), src=(3, 1), det=(2, 2), eps=0.4),
          3: dict(n=(7, 7, 5), src=(2, 1), det=(2, 2), eps=0.4)}
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, sketch=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     tdist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1706_05586_b200.sharded import ShardPlan, sharded_step
@@ -82,14 +82,18 @@ def _worker(rank, world, port, out):
     W = np.sign(rng.standard_normal((cfg.n_s, 2)))
     V = np.sign(rng.standard_normal((cfg.n_d, 3)))
     plan = ShardPlan(rank, world, cfg.n_s, cfg.n_d)
+    if not sketch:                       # the all-sources step of configs[4]: no sketch, full J only
+        W = V = None
     try:
-        r = sharded_step(OracleBackend(prob), plan, torch.as_tensor(wl.p), torch.as_tensor(W), torch.as_tensor(V),
+        r = sharded_step(OracleBackend(prob), plan, torch.as_tensor(wl.p),
+                         None if W is None else torch.as_tensor(W), None if V is None else torch.as_tensor(V),
                          device=torch.device("cpu"))
     except Exception as e:  # report instead of hanging the parent
         out.put(("error", repr(e)))
         raise
     if rank == 0:
-        out.put((r["misfit"], np.asarray(r["J_full"]), np.asarray(r["J_sketch"]), prob.solves))
+        out.put((r["misfit"], np.asarray(r["J_full"]), None if r["J_sketch"] is None else np.asarray(r["J_sketch"]),
+                 prob.solves))
     else:
         out.put(("solves", prob.solves))
     tdist.barrier()
@@ -123,6 +127,30 @@ def test_sharded_step_equals_unsharded(world):
     assert np.abs(Jf - Jf_ref).max() <= 1e-10 * np.abs(Jf_ref).max()
     Js_ref = jacobian(prob, wl.p, W, V)
     assert np.abs(Js - Js_ref).max() <= 1e-10 * np.abs(Js_ref).max()
+
+
+def test_all_sources_step_shape_two_ranks():
+    """The bench's configs[4] step (`--config all128 --gpus N`): no sketch, misfit and the full
+    Jacobian gathered on rank 0, world 2 on gloo."""
+    from oracle import jacobian, misfit
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, False)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert not [r for r in res if r[0] == "error"], res
+    m, Jf, Js, _ = [r for r in res if r[0] != "solves"][0]
+    assert Js is None
+    cfg = small_config(**CASES[2])
+    prob, wl = small_problem(cfg)
+    assert m == pytest.approx(misfit(prob, wl.p, np.eye(cfg.n_s), np.eye(cfg.n_d)), rel=1e-10)
+    Jf_ref = jacobian(prob, wl.p, np.eye(cfg.n_s), np.eye(cfg.n_d))
+    assert np.abs(Jf - Jf_ref).max() <= 1e-10 * np.abs(Jf_ref).max()
 
 
 def test_shard_plan_blocks_cover_once():

@@ -15,6 +15,6 @@ timeout 600 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 600 $PCMD > gpurun_out/plain2.log 2>&1 && \
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:cg_pass_kernel -s 420 -c 1 -o gpurun_out/prof_pass $PCMD > gpurun_out/ncu_pass.log 2>&1; echo "ncu pass rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:contract -c 2 -o gpurun_out/prof_contract $PCMD > gpurun_out/ncu_contract.log 2>&1; echo "ncu contract rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:contract_seg -c 1 -o gpurun_out/prof_contract $PCMD > gpurun_out/ncu_contract.log 2>&1; echo "ncu contract rc=$?"
 python tools/sass_mix.py gpurun_out/prof_pass.ncu-rep > gpurun_out/sass_mix.txt 2>&1
 ls -la gpurun_out
