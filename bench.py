@@ -375,7 +375,8 @@ def main():
         W_h = pin(wl.W) if wl.W is not None else None
         V_h = pin(wl.V) if wl.V is not None else None
         h2d = p_h.nbytes + D_h.nbytes + (W_h.nbytes if W_h is not None else 0) + (V_h.nbytes if V_h is not None else 0)
-        run_step(p_h, W_h, V_h, data=D_h)                         # warm
+        for _ in range(2):                                        # warm (pinned result buffers cached)
+            run_step(p_h, W_h, V_h, data=D_h)
         barrier()
         t0 = time.perf_counter()
         e2e_ev0 = torch.cuda.Event(enable_timing=True)
@@ -387,6 +388,7 @@ def main():
                 flush.zero_()                                     # same L2 hygiene as the device-timed loop
             r = run_step(p_h, W_h, V_h, data=D_h)
             d2h = r["d2h_bytes"]
+            r = None                                              # results consumed: buffers reusable
         e2e_ev1.record(stream)
         barrier()
         e_ms = e2e_ev0.elapsed_time(e2e_ev1) / args.steps

@@ -1455,15 +1455,13 @@ int dot_optimize_directions_subspace(dot_problem* P, int32_t k, int32_t iters, i
     const int nf = P->n_freq, K = P->K, nP = P->nP;
     cudaStream_t s = P->stream;
     SubspaceOps ops;
-    ops.fields = [&](int side, const std::vector<double>& coeff, int ncols, double2* out) {
-        DBuf<double> dc = to_device(P, coeff.data(), coeff.size(), DOT_HOST);
+    ops.fields = [&](int side, const double* d_coeff, int ncols, double2* out) {
         DBuf<double2> XP(P->arena, std::max<size_t>((size_t)nf * ncols * nP, 1));
-        solve_batch(P, {Seg{side, dc.get(), ncols}}, nullptr, {}, XP.get(), nf * ncols, nP, P->d_P.get(),
+        solve_batch(P, {Seg{side, d_coeff, ncols}}, nullptr, {}, XP.get(), nf * ncols, nP, P->d_P.get(),
                     P->d_off.get());
         launch_gather_cols(nf, ncols, K, XP.get(), (size_t)ncols * nP, nP, P->d_S_slot.get(), out, (size_t)ncols * K,
                            K, s);
         P->stats.kernel_launches++;
-        sync(P);
     };
     ops.solve_support = [&](const double2* w, int nvec, int side, double2* out) {
         const int nr = nf * nvec;
@@ -1477,20 +1475,9 @@ int dot_optimize_directions_subspace(dot_problem* P, int32_t k, int32_t iters, i
         const int n_side = side == 0 ? P->n_src : P->n_det;
         launch_gather_cols(nf, nvec, n_side, XP.get(), (size_t)nvec * nP, nP,
                            side == 0 ? P->d_src_slot.get() : P->d_det_slot.get(), out, (size_t)nvec * n_side, n_side, s);
-        P->stats.kernel_launches += 2;
-        if (side == 0) {     // b_s^T x = theta_s / (hx hy hz) x[src_s]  (reading R6)
-            std::vector<double2> h((size_t)nr * n_side);
-            DOT_CUDA_TRY(cudaMemcpyAsync(h.data(), out, h.size() * sizeof(double2), cudaMemcpyDeviceToHost, s));
-            sync(P);
-            for (int r = 0; r < nr; ++r)
-                for (int a = 0; a < n_side; ++a) {
-                    double2& v = h[(size_t)r * n_side + a];
-                    v.x *= P->src_scale[a];
-                    v.y *= P->src_scale[a];
-                }
-            DOT_CUDA_TRY(cudaMemcpyAsync(out, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
-        }
-        sync(P);
+        // b_s^T x = theta_s / (hx hy hz) x[src_s]  (reading R6), on the device
+        if (side == 0) launch_scale_cols(out, (size_t)nr, n_side, P->d_src_scale.get(), s);
+        P->stats.kernel_launches += side == 0 ? 3 : 2;
     };
     OptContext oc{P->arena, P->stream, P->n_freq, P->n_src, P->n_det, P->n_p, P->K, P->nP,
                   nullptr, nullptr, P->d_S_slot.get(), P->d_G.get(), &P->stats.kernel_launches, &P->gsp};

@@ -151,6 +151,8 @@ void launch_rc_gemm(int nb, int M, int N, int K, const double* Rm, int ldr, cons
 // out[b][i][j] = X[b][i][idx[j]] (gather columns)
 void launch_gather_cols(int nb, int rows, int ncols, const double2* X, size_t xb, size_t xr,
                         const int32_t* idx, double2* out, size_t ob, size_t orow, cudaStream_t s);
+// X[r][c] *= scale[c] (complex X [rows][ncols], real scale)
+void launch_scale_cols(double2* X, size_t rows, int ncols, const double* scale, cudaStream_t s);
 // a[i] -= b[i] (complex)
 void launch_csub_inplace(double2* a, const double2* b, size_t n, cudaStream_t s);
 // a[i] += b[i] (complex)

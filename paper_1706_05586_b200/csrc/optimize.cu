@@ -54,6 +54,99 @@ __global__ void __launch_bounds__(256) gram_kernel(const double2* __restrict__ X
         }
 }
 
+// device helpers of the matrix-free add step (n x cols row-major real blocks) --------------
+__device__ double block_sum(double v, double* red) {     // result valid in every thread
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double t = 0;
+    for (int w = 0; w < nw; ++w) t += red[w];     // fixed order: every thread the same value
+    return t;
+}
+
+// X[:, j] <- (I - QM QM^T) X[:, j] for every column j (QM: n x l orthonormal, l <= 32); one block
+// per column
+__global__ void __launch_bounds__(256) proj_complement_kernel(const double* QM, int n, int l, double* X, int cols) {
+    __shared__ double red[8], d[32];
+    const int j = blockIdx.x;
+    for (int p = 0; p < l; ++p) {
+        double v = 0;
+        for (int r = threadIdx.x; r < n; r += blockDim.x) v += QM[(size_t)r * l + p] * X[(size_t)r * cols + j];
+        v = block_sum(v, red);
+        if (threadIdx.x == 0) d[p] = v;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+        double x = X[(size_t)r * cols + j];
+        for (int p = 0; p < l; ++p) x -= d[p] * QM[(size_t)r * l + p];
+        X[(size_t)r * cols + j] = x;
+    }
+}
+
+// orthonormal basis of the columns of X in place: modified Gram-Schmidt, two passes (one block);
+// *fail = 1 for a zero column
+__global__ void __launch_bounds__(1024) mgs_kernel(double* X, int n, int cols, int* fail) {
+    __shared__ double red[32];
+    for (int j = 0; j < cols; ++j) {
+        for (int pass = 0; pass < 2; ++pass)
+            for (int i = 0; i < j; ++i) {
+                double v = 0;
+                for (int r = threadIdx.x; r < n; r += blockDim.x) v += X[(size_t)r * cols + i] * X[(size_t)r * cols + j];
+                v = block_sum(v, red);
+                for (int r = threadIdx.x; r < n; r += blockDim.x) X[(size_t)r * cols + j] -= v * X[(size_t)r * cols + i];
+                __syncthreads();
+            }
+        double v = 0;
+        for (int r = threadIdx.x; r < n; r += blockDim.x) v += X[(size_t)r * cols + j] * X[(size_t)r * cols + j];
+        const double nr = sqrt(block_sum(v, red));
+        if (nr == 0.0) {
+            if (threadIdx.x == 0) *fail = 1;
+            return;
+        }
+        for (int r = threadIdx.x; r < n; r += blockDim.x) X[(size_t)r * cols + j] /= nr;
+        __syncthreads();
+    }
+}
+
+// C[f][q][i][k] = conj(T) with T = J[f][i][q][k] (side 0: J = [nf][nF][blk][n_p]) or
+// J[f][q][i][k] (side 1: J = [nf][blk][nF][n_p])
+__global__ void conj_reorder_kernel(const double2* J, int nf, int blk, int nF, int n_p, int side, double2* C) {
+    const size_t tot = (size_t)nf * blk * nF * n_p;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
+        const int kk = (int)(e % n_p);
+        size_t t = e / n_p;
+        const int i = (int)(t % nF);
+        t /= nF;
+        const int q = (int)(t % blk);
+        const int f = (int)(t / blk);
+        const size_t src = side == 0 ? (((size_t)f * nF + i) * blk + q) * n_p + kk : (((size_t)f * blk + q) * nF + i) * n_p + kk;
+        const double2 v = J[src];
+        C[e] = make_double2(v.x, -v.y);
+    }
+}
+
+// Y[r][q] = - sum_f Re(out[f][q][r])
+__global__ void neg_re_sum_kernel(const double2* out, int nf, int blk, int n, double* Y) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * blk; e += gridDim.x * blockDim.x) {
+        const int r = e / blk, q = e % blk;
+        double v = 0;
+        for (int f = 0; f < nf; ++f) v -= out[((size_t)f * blk + q) * n + r].x;
+        Y[e] = v;
+    }
+}
+
+// H[i][j] = sum_r A[r][i] B[r][j] (n x c blocks); one block per entry
+__global__ void __launch_bounds__(256) small_atb_kernel(const double* A, const double* B, int n, int c, double* H) {
+    __shared__ double red[8];
+    const int i = blockIdx.x / c, j = blockIdx.x % c;
+    double v = 0;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) v += A[(size_t)r * c + i] * B[(size_t)r * c + j];
+    v = block_sum(v, red);
+    if (threadIdx.x == 0) H[blockIdx.x] = v;
+}
+
 // host helpers ----------------------------------------------------------------
 std::vector<double> matmul(const std::vector<double>& A, int m, int k, const std::vector<double>& B, int n) {
     std::vector<double> C((size_t)m * n, 0.0);
@@ -246,13 +339,20 @@ double optimize_two_phase_subspace(OptContext& c, SubspaceOps& ops, int k, int i
     const int nf = c.nf, ns = c.ns, nd = c.nd, n_p = c.n_p, K = c.K;
     cudaStream_t s = c.stream;
     auto sync = [&]() { DOT_CUDA_TRY(cudaStreamSynchronize(s)); };
-    auto fields = [&](int side, const std::vector<double>& coeff, int ncols) {
+    auto fields = [&](int side, const double* d_coeff, int ncols) {     // device coefficients
         DBuf<double2> out(c.arena, std::max<size_t>((size_t)nf * ncols * K, 1));
-        ops.fields(side, coeff, ncols, out.get());
+        ops.fields(side, d_coeff, ncols, out.get());
+        return out;
+    };
+    auto fields_h = [&](int side, const std::vector<double>& coeff, int ncols) {
+        DBuf<double> dc(c.arena, std::max<size_t>(coeff.size(), 1));
+        DOT_CUDA_TRY(cudaMemcpyAsync(dc.get(), coeff.data(), coeff.size() * 8, cudaMemcpyHostToDevice, s));
+        DBuf<double2> out = fields(side, dc.get(), ncols);
+        sync();
         return out;
     };
     // z fields of W and y fields of V on S: [nf][cols][K]
-    DBuf<double2> ZW = fields(0, W, ls), YV = fields(1, V, ld);
+    DBuf<double2> ZW = fields_h(0, W, ls), YV = fields_h(1, V, ld);
     int a = ls, b = ld;
 
     auto contract = [&](const double2* lam, int nl, const double2* u, int nu) {
@@ -260,12 +360,6 @@ double optimize_two_phase_subspace(OptContext& c, SubspaceOps& ops, int k, int i
         launch_contract(nf, K, nl, nu, n_p, lam, (size_t)nl * K, u, (size_t)nu * K, c.G, J.get(), s, c.gsp);
         *c.launches += 1;
         return J;
-    };
-    auto to_host = [&](const double2* d, size_t n) {
-        std::vector<double2> h(n);
-        DOT_CUDA_TRY(cudaMemcpyAsync(h.data(), d, n * sizeof(double2), cudaMemcpyDeviceToHost, s));
-        sync();
-        return h;
     };
     // new fields F' [nf][m][K] = sum_j Gam[j][m] F[f][j][K]  (Gam host [ncols][m])
     auto combine = [&](const DBuf<double2>& F, int ncols, const std::vector<double>& Gam, int m) {
@@ -319,70 +413,72 @@ double optimize_two_phase_subspace(OptContext& c, SubspaceOps& ops, int k, int i
     }
 
     // ---- one matrix-free add step.  side 0: new source (kept fields F = YV, b cols);
-    // side 1: new detector (kept fields F = ZW, a cols).  M = current directions.
+    // side 1: new detector (kept fields F = ZW, a cols).  M = current directions.  The block
+    // Q, its image Y = K Q, the projection onto the complement of span(M) and the
+    // orthonormalisation stay on the device; only the blk x blk Rayleigh-Ritz matrix and the
+    // final block come to the host.
+    DBuf<int> dfail(c.arena, 1);
+    DOT_CUDA_TRY(cudaMemsetAsync(dfail.get(), 0, sizeof(int), s));
     auto add_step = [&](int side, std::vector<double>& M, int l, const DBuf<double2>& F, int nF,
                         const std::vector<double>& X0all, int step, DBuf<double2>& newfield) {
         const int n = side == 0 ? ns : nd;
-        const std::vector<double> QM = orth_basis(M, n, l);
-        auto project = [&](std::vector<double>& X, int cols) {      // X <- (I - QM QM^T) X
-            for (int j = 0; j < cols; ++j)
-                for (int p = 0; p < l; ++p) {
-                    double d = 0;
-                    for (int r = 0; r < n; ++r) d += QM[(size_t)r * l + p] * X[(size_t)r * cols + j];
-                    for (int r = 0; r < n; ++r) X[(size_t)r * cols + j] -= d * QM[(size_t)r * l + p];
-                }
+        const std::vector<double> QMh = orth_basis(M, n, l);
+        DBuf<double> QM(c.arena, QMh.size()), dQ(c.arena, (size_t)n * blk), dY(c.arena, (size_t)n * blk);
+        DOT_CUDA_TRY(cudaMemcpyAsync(QM.get(), QMh.data(), QMh.size() * 8, cudaMemcpyHostToDevice, s));
+        auto project = [&](double* X) {                            // X <- (I - QM QM^T) X
+            proj_complement_kernel<<<blk, 256, 0, s>>>(QM.get(), n, l, X, blk);
+            DOT_CUDA_TRY(cudaGetLastError());
+            *c.launches += 1;
         };
-        // K Q (Q: n x blk, already in range(P)); also returns the fields of Q on S
-        auto applyK = [&](const std::vector<double>& Q, DBuf<double2>& FQ) {
-            FQ = fields(side, Q, blk);                                  // [nf][blk][K]
-            // T[f][..] = Xr^T q in complex form
+        auto orth = [&](double* X) {
+            mgs_kernel<<<1, 1024, 0, s>>>(X, n, blk, dfail.get());
+            DOT_CUDA_TRY(cudaGetLastError());
+            *c.launches += 1;
+        };
+        // Y = K Q (Q: n x blk in range(P)); FQ receives the fields of Q on S
+        auto applyK = [&](DBuf<double2>& FQ) {
+            FQ = fields(side, dQ.get(), blk);                               // [nf][blk][K]
+            // T[f][..] = Xr^T q in complex form; coefficients C[f][q][i][k] = conj(T)
             DBuf<double2> J = side == 0 ? contract(F.get(), nF, FQ.get(), blk)    // [nf][nF][blk][n_p]
                                         : contract(FQ.get(), blk, F.get(), nF);   // [nf][blk][nF][n_p]
-            std::vector<double2> T = to_host(J.get(), (size_t)nf * nF * blk * n_p);
-            // coefficients C[f][q][i][k] = conj(T)
-            std::vector<double2> Cc((size_t)nf * blk * nF * n_p);
-            for (int f = 0; f < nf; ++f)
-                for (int q = 0; q < blk; ++q)
-                    for (int i = 0; i < nF; ++i)
-                        for (int kk = 0; kk < n_p; ++kk) {
-                            const size_t src = side == 0 ? (((size_t)f * nF + i) * blk + q) * n_p + kk
-                                                         : (((size_t)f * blk + q) * nF + i) * n_p + kk;
-                            const double2 t = T[src];
-                            Cc[(((size_t)f * blk + q) * nF + i) * n_p + kk] = make_double2(t.x, -t.y);
-                        }
-            DBuf<double2> dC(c.arena, Cc.size()), w(c.arena, std::max<size_t>((size_t)nf * blk * K, 1));
-            DOT_CUDA_TRY(cudaMemcpyAsync(dC.get(), Cc.data(), Cc.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+            const size_t nC = (size_t)nf * blk * nF * n_p;
+            DBuf<double2> dC(c.arena, std::max<size_t>(nC, 1)), w(c.arena, std::max<size_t>((size_t)nf * blk * K, 1));
+            conj_reorder_kernel<<<(unsigned)std::min<size_t>((nC + 255) / 256, 1024), 256, 0, s>>>(J.get(), nf, blk,
+                                                                                                nF, n_p, side, dC.get());
+            DOT_CUDA_TRY(cudaGetLastError());
             launch_form_support_rhs(nf, blk, K, nF, n_p, dC.get(), F.get(), c.G, w.get(), s);
-            *c.launches += 1;
             DBuf<double2> out(c.arena, (size_t)nf * blk * n);
             ops.solve_support(w.get(), blk, side, out.get());
-            std::vector<double2> hs = to_host(out.get(), (size_t)nf * blk * n);
-            std::vector<double> Y((size_t)n * blk, 0.0);
-            for (int f = 0; f < nf; ++f)
-                for (int q = 0; q < blk; ++q)
-                    for (int r = 0; r < n; ++r) Y[(size_t)r * blk + q] -= hs[((size_t)f * blk + q) * n + r].x;
-            project(Y, blk);
-            return Y;
+            neg_re_sum_kernel<<<(n * blk + 255) / 256, 256, 0, s>>>(out.get(), nf, blk, n, dY.get());
+            DOT_CUDA_TRY(cudaGetLastError());
+            *c.launches += 3;
+            project(dY.get());
         };
-        std::vector<double> Q((size_t)n * blk);              // start block of this add step
+        std::vector<double> Q0((size_t)n * blk);              // start block of this add step
         for (int r = 0; r < n; ++r)
-            for (int j = 0; j < blk; ++j) Q[(size_t)r * blk + j] = X0all[(size_t)r * k * blk + step * blk + j];
-        project(Q, blk);
-        Q = orth_basis(Q, n, blk);
+            for (int j = 0; j < blk; ++j) Q0[(size_t)r * blk + j] = X0all[(size_t)r * k * blk + step * blk + j];
+        DOT_CUDA_TRY(cudaMemcpyAsync(dQ.get(), Q0.data(), Q0.size() * 8, cudaMemcpyHostToDevice, s));
+        project(dQ.get());
+        orth(dQ.get());
         DBuf<double2> FQ;
-        std::vector<double> Y = applyK(Q, FQ);
+        applyK(FQ);
         for (int t = 1; t < iters; ++t) {
-            Q = orth_basis(Y, n, blk);
-            Y = applyK(Q, FQ);
+            DOT_CUDA_TRY(cudaMemcpyAsync(dQ.get(), dY.get(), (size_t)n * blk * 8, cudaMemcpyDeviceToDevice, s));
+            orth(dQ.get());
+            applyK(FQ);
         }
-        // Rayleigh-Ritz: H = Q^T Y, top eigenvector e, q = Q e
-        std::vector<double> H((size_t)blk * blk, 0.0);
-        for (int i = 0; i < blk; ++i)
-            for (int j = 0; j < blk; ++j) {
-                double d = 0;
-                for (int r = 0; r < n; ++r) d += Q[(size_t)r * blk + i] * Y[(size_t)r * blk + j];
-                H[(size_t)i * blk + j] = d;
-            }
+        // Rayleigh-Ritz: H = Q^T Y (device), top eigenvector e (host), q = Q e
+        DBuf<double> dH(c.arena, (size_t)blk * blk);
+        small_atb_kernel<<<blk * blk, 256, 0, s>>>(dQ.get(), dY.get(), n, blk, dH.get());
+        DOT_CUDA_TRY(cudaGetLastError());
+        *c.launches += 1;
+        std::vector<double> H((size_t)blk * blk), Q((size_t)n * blk);
+        int failed = 0;
+        DOT_CUDA_TRY(cudaMemcpyAsync(H.data(), dH.get(), H.size() * 8, cudaMemcpyDeviceToHost, s));
+        DOT_CUDA_TRY(cudaMemcpyAsync(Q.data(), dQ.get(), Q.size() * 8, cudaMemcpyDeviceToHost, s));
+        DOT_CUDA_TRY(cudaMemcpyAsync(&failed, dfail.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+        sync();
+        if (failed) throw Error(DOT_ERR_ARG, "subspace block is rank deficient");
         for (int i = 0; i < blk; ++i)
             for (int j = i + 1; j < blk; ++j) H[(size_t)i * blk + j] = H[(size_t)j * blk + i] =
                 0.5 * (H[(size_t)i * blk + j] + H[(size_t)j * blk + i]);
@@ -397,12 +493,12 @@ double optimize_two_phase_subspace(OptContext& c, SubspaceOps& ops, int k, int i
         nr = std::sqrt(nr);
         const double sgn = q[imax] >= 0 ? 1.0 : -1.0;              // largest entry positive (oracle rule)
         const double scale = sgn * std::sqrt((double)n) / nr;      // length sqrt(n) (reading R15)
-        std::vector<double> out((size_t)n * (l + 1));
+        std::vector<double> outM((size_t)n * (l + 1));
         for (int r = 0; r < n; ++r) {
-            for (int j = 0; j < l; ++j) out[(size_t)r * (l + 1) + j] = M[(size_t)r * l + j];
-            out[(size_t)r * (l + 1) + l] = scale * q[r];
+            for (int j = 0; j < l; ++j) outM[(size_t)r * (l + 1) + j] = M[(size_t)r * l + j];
+            outM[(size_t)r * (l + 1) + l] = scale * q[r];
         }
-        M.swap(out);
+        M.swap(outM);
         // fields of the new column from the last block's fields (no extra solve)
         std::vector<double> ge(blk);
         for (int j = 0; j < blk; ++j) ge[j] = scale * e[j];

@@ -25,11 +25,11 @@ struct OptContext {
 double optimize_two_phase(OptContext& c, int k, std::vector<double>& W, int ls, std::vector<double>& V, int ld);
 
 // Solver callbacks of the matrix-free (subspace-iteration) variant, provided by the
-// C-ABI layer (they run the batched COCG kernels):
+// C-ABI layer (they run the batched multi-shift CG kernels; no host synchronisation needed):
 struct SubspaceOps {
     // fields of point combinations on the support S: side 0 = B coeff (sources), 1 = C coeff
-    // (detectors); coeff host [n_side][ncols] row-major; out device [nf][ncols][K]
-    std::function<void(int side, const std::vector<double>& coeff, int ncols, double2* out)> fields;
+    // (detectors); coeff device [n_side][ncols] row-major; out device [nf][ncols][K]
+    std::function<void(int side, const double* d_coeff, int ncols, double2* out)> fields;
     // solve A_f x = w_f for nvec right-hand sides supported on S (w device [nf][nvec][K]) and
     // return b_s^T x (side 0, sources; b_s = theta e_s / cell volume) or c_d^T x (side 1):
     // out device [nf][nvec][n_side]

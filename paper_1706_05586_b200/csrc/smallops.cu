@@ -106,6 +106,14 @@ inline unsigned blocks_for(size_t n) {
     return (unsigned)std::max<size_t>(1, std::min<size_t>(g, 8192));
 }
 
+__global__ void scale_cols_kernel(double2* X, size_t rows, int ncols, const double* scale) {
+    const size_t tot = rows * ncols;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
+        const double sc = scale[e % ncols];
+        X[e] = make_double2(X[e].x * sc, X[e].y * sc);
+    }
+}
+
 }  // namespace
 
 void launch_rc_gemm(int nb, int M, int N, int K, const double* Rm, int ldr, const double2* Cx,
@@ -159,6 +167,13 @@ void launch_form_support_rhs(int nf, int nq, int K, int ncol, int n_p, const dou
     if (nf <= 0 || nq <= 0 || K <= 0) return;
     dim3 grid((unsigned)std::min((K + 127) / 128, 1024), nq, nf);
     form_support_rhs_kernel<<<grid, 128, 0, s>>>(K, ncol, n_p, nq, C, Z, G, w);
+    DOT_CUDA_TRY(cudaGetLastError());
+}
+
+void launch_scale_cols(double2* X, size_t rows, int ncols, const double* scale, cudaStream_t s) {
+    const size_t tot = rows * ncols;
+    if (!tot) return;
+    scale_cols_kernel<<<(unsigned)std::min<size_t>((tot + 255) / 256, 1024), 256, 0, s>>>(X, rows, ncols, scale);
     DOT_CUDA_TRY(cudaGetLastError());
 }
 
