@@ -242,13 +242,21 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, c
         if (e) {
             n = std::min(std::max(1, std::atoi(e)), std::max(1, P->nz / 4));
         } else {
-            // measured (tools/pass_bench.py, round 2): opt96 at 12 pairs 0.41 / 0.51 / 0.47 of the HBM
-            // peak with 1 / 2 / 4 chunks; sketch32 at 8 pairs 0.06 / 0.09 / 0.13 -- two waves of CTAs,
-            // chunks of >= 8 planes
-            const long long target = 2LL * P->num_sms;
+            // wave model: a pass costs ~ ceil(CTAs / SMs) waves x (planes per chunk + 4 halo planes +
+            // ~2 planes of start-up); pick the chunk count that minimises it (chunks >= 8 planes).
+            // Measured (tools/pass_bench.py): opt96 at 12 pairs 0.41 / 0.51 / 0.47 of the HBM peak with
+            // 1 / 2 / 4 chunks -- the model's choice is 2.
             const long long have = (long long)P->tl.ntiles * nb;
-            if (have < target && P->nz >= 32) n = (int)((target + have - 1) / have);
-            n = std::min(n, std::max(1, P->nz / 8));
+            const int nmax = std::max(1, P->nz / 8);
+            double best = 0;
+            for (int c = 1; c <= nmax; ++c) {
+                const long long waves = (have * c + P->num_sms - 1) / P->num_sms;
+                const double t = (double)waves * ((P->nz + c - 1) / c + 6);
+                if (c == 1 || t < best - 1e-9) {
+                    best = t;
+                    n = c;
+                }
+            }
         }
         const int zlen = (P->nz + n - 1) / n;
         return (P->nz + zlen - 1) / zlen;
