@@ -448,7 +448,7 @@ def main():
                    "solves_per_step": solves_per_step, "parallelism": f"rhs-shard x{world}",
                    "l2": (f"working set ~{ws_bytes / 1e9:.1f} GB >> 126 MB L2 (no flush needed)" if flush is None
                           else f"working set ~{ws_bytes / 1e6:.0f} MB: 256 MB L2 flush between timed steps"),
-                   "cocg_tol": 1e-17},
+                   "cg_tol": gp.tol if hasattr(gp, "tol") else 1e-17},
         "krylov_iterations_per_s": (st["rhs_iterations"] - s0["rhs_iterations"]) / args.steps / (ms / 1e3),
         "seed_solves_per_step": (st["seeds_solved"] - s0["seeds_solved"]) / args.steps,
         "seed_iterations_per_s": (st["seed_iterations"] - s0["seed_iterations"]) / args.steps / (ms / 1e3),

@@ -46,7 +46,7 @@ extern "C" {
 #define DOT_ERR_STATE 3      /* call order (e.g. misfit before set_params)   */
 #define DOT_ERR_NOCONV 4     /* a Krylov solve hit max_iter                  */
 #define DOT_ERR_WORKSPACE 5  /* bound workspace too small for the request    */
-#define DOT_ERR_BREAKDOWN 6  /* COCG breakdown (p^T A p = 0 or non-finite)   */
+#define DOT_ERR_BREAKDOWN 6  /* CG breakdown (p^T K p <= 0 or non-finite)     */
 
 #define DOT_HOST 0
 #define DOT_DEVICE 1
@@ -71,8 +71,8 @@ typedef struct dot_config {
     double gamma;                /* ||x||^dagger regulariser              */
     double eps;                  /* smoothed-Heaviside half width (reading R8)            */
     double cutoff;               /* level-set cut-off c (Eq. (2.4))                       */
-    double tol;                  /* COCG stop: ||r_k||_2 <= tol ||b||_2 (reading R12); <=0: 1e-17 */
-    int32_t max_iter;            /* COCG iteration cap; <= 0: 4000                        */
+    double tol;                  /* Krylov stop per system: ||r_sigma||_2 <= tol ||b||_2 (reading R12); <=0: 1e-17 */
+    int32_t max_iter;            /* Krylov iteration cap; <= 0: 4000                      */
 } dot_config;
 
 typedef struct dot_stats {
@@ -116,7 +116,7 @@ size_t dot_workspace_bytes(const dot_problem* P, int32_t max_rhs);
 /* Bind caller-owned device memory (>= dot_workspace_bytes(P, 1)).  Rebinding
  * invalidates parameters, data and cached fields. */
 int dot_bind_workspace(dot_problem* P, void* dev_ptr, size_t bytes);
-/* Enable CUDA-event timing of the COCG pass and contraction kernels (dot_stats). */
+/* Enable CUDA-event timing of the CG pass and contraction kernels (dot_stats). */
 int dot_enable_timing(dot_problem* P, int on);
 int dot_get_stats(const dot_problem* P, dot_stats* out);
 int dot_reset_stats(dot_problem* P);
@@ -245,8 +245,11 @@ int dot_absorption(dot_problem* P, double* mu_out, int where);
 int dot_support(dot_problem* P, int32_t* K_out, int64_t* nodes_out, double* G_out, int where);
 /* Au = A(omega_f, p) u for nrhs fields: u, Au [nrhs][N] complex. */
 int dot_apply(dot_problem* P, int32_t freq, int32_t nrhs, const double* u, double* Au, int where);
-/* Solve A(omega_{freq[r]}, p) x_r = b_r with the fused COCG kernels: b, x [nrhs][N]
- * complex; freq [nrhs] int32 (same `where`).  iters_out (host, may be NULL) [nrhs]. */
+/* Solve A(omega_{freq[r]}, p) x_r = b_r (Eq. (2.1)) with the multi-shift CG kernels
+ * (Re b_r and Im b_r are two real seeds at shift omega_{freq[r]}/nu, every node sampled):
+ * b, x [nrhs][N] complex; freq [nrhs] int32 (same `where`).  iters_out (host, may be NULL)
+ * [nrhs]: iterations of the slower seed.  Dense-output test/diagnostic call: the workspace
+ * of dot_workspace_bytes covers up to 3 right-hand sides per call. */
 int dot_solve(dot_problem* P, int32_t nrhs, const int32_t* freq, const double* b, double* x,
               int where, int32_t* iters_out);
 /* Sampled solve of point-source / point-detector combinations: side 0 = sources

@@ -92,6 +92,7 @@ class DOTProblem:
             raise RuntimeError("DOTProblem needs a CUDA device (B200); there is no CPU path")
         self.n = tuple(int(v) for v in n)
         self.N = self.n[0] * self.n[1] * self.n[2]
+        self.tol = float(tol)
         self.omegas = np.ascontiguousarray(np.asarray(omegas, dtype=np.float64))
         self.src_nodes = np.ascontiguousarray(np.asarray(src_nodes, dtype=np.int64))
         self.det_nodes = np.ascontiguousarray(np.asarray(det_nodes, dtype=np.int64))
