@@ -1117,8 +1117,9 @@ int dot_create(const dot_config* cfg, dot_problem** out) {
             const char* ePD = std::getenv("DOT_CG_PREFETCH");
             const char* eTY = std::getenv("DOT_CG_TY");
             const char* eRW = std::getenv("DOT_CG_ROWS");
+            const char* eNM = std::getenv("DOT_CG_NOMU");
             P->tl = cg_tiling(P->nx, P->ny, P->nz, ePD ? std::max(1, std::atoi(ePD)) : 2, eTY ? std::atoi(eTY) : 0,
-                              eRW ? std::atoi(eRW) : 0);
+                              eRW ? std::atoi(eRW) : 0, eNM && std::atoi(eNM) != 0);
         }
         P->pc = PalsConst{P->nx, P->ny, P->nz, P->n_rbf, P->hx, P->hy, P->hz, P->gamma, P->eps, P->cutoff,
                           P->mua_in, P->mua_out};

@@ -856,9 +856,9 @@ __global__ void pack_planes_kernel(const double2* A, const double2* B, size_t N,
 
 }  // namespace
 
-size_t pass_smem(int nx, int TY, int NS, int nz) {
+size_t pass_smem(int nx, int TY, int NS, int nz, bool mut) {
     const size_t slotE = (size_t)(TY + 4) * nx;
-    const size_t e = (size_t)NS * (2 * slotE + (nx % 2 == 0 ? (slotE + 1) / 2 : 0)) + 3 * (size_t)(TY + 2) * nx;
+    const size_t e = (size_t)NS * (2 * slotE + (mut ? (slotE + 1) / 2 : 0)) + 3 * (size_t)(TY + 2) * nx;
     return e * sizeof(double2) + (NS + 2) * 8 + 32 * kNumPartials * 8 + 8 * (size_t)nz + 128;
 }
 
@@ -866,7 +866,8 @@ size_t pass_smem(int nx, int TY, int NS, int nz) {
 //   2 rows per thread, <= 512 threads (default);  1 row per thread, <= 512 threads (fallback)
 // DOT_CG_TY forces the tile height, DOT_CG_ROWS the rows per thread, DOT_CG_PREFETCH the TMA
 // depth (1..3) -- test knobs.
-CgTiling cg_tiling(int nx, int ny, int nz, int prefetch, int want_ty, int want_rows) {
+CgTiling cg_tiling(int nx, int ny, int nz, int prefetch, int want_ty, int want_rows, bool no_mu) {
+    const bool mut = (nx % 2 == 0) && !no_mu;    // mu in the slots needs 16-byte rows
     const int NS = std::max(1, std::min(prefetch, 3)) + 2;
     const size_t sm_cta = 227 * 1024;
     struct Opt { int rows, maxt; };
@@ -878,7 +879,7 @@ CgTiling cg_tiling(int nx, int ny, int nz, int prefetch, int want_ty, int want_r
         int ty = 0;
         for (int c = 1; c <= ny; ++c) {
             const int thr = ((c + 4 + o.rows - 1) / o.rows * nx + 31) / 32 * 32;
-            if (thr > o.maxt || pass_smem(nx, c, NS, nz) > sm_cta) break;
+            if (thr > o.maxt || pass_smem(nx, c, NS, nz, mut) > sm_cta) break;
             ty = c;
             if (want_ty > 0 && c == want_ty) break;
         }
@@ -891,7 +892,8 @@ CgTiling cg_tiling(int nx, int ny, int nz, int prefetch, int want_ty, int want_r
         t.ntiles = (ny + t.TY - 1) / t.TY;
         t.nslots = NS;
         t.threads = ((t.TY + 4 + o.rows - 1) / o.rows * nx + 31) / 32 * 32;
-        t.smem = pass_smem(nx, t.TY, NS, nz);
+        t.smem = pass_smem(nx, t.TY, NS, nz, mut);
+        t.mut = mut;
         if (!found || (best.TY < 4 && t.TY > best.TY)) {
             best = t;
             found = true;
@@ -905,7 +907,7 @@ CgTiling cg_tiling(int nx, int ny, int nz, int prefetch, int want_ty, int want_r
 template <int MAXT, int NS, int RPT>
 static void launch_pass_ns(const PassArgs& a, int nb, cudaStream_t s) {
     // mu rides in the bulk-copy group when every copy is 16-byte sized and aligned
-    const bool mut = (a.op.nx % 2 == 0);
+    const bool mut = a.tl.mut;
     const bool zc = a.nzch > 1 || a.nzch_tot > 1;
     using KF = void (*)(const PassArgs);
     KF k = mut ? (zc ? cg_pass_kernel<MAXT, NS, true, RPT, true, 0, 0> : cg_pass_kernel<MAXT, NS, true, RPT, false, 0, 0>)

@@ -11,13 +11,14 @@ namespace dot {
 // copies into a ring of `nslots` shared-memory slots.
 struct CgTiling {
     int rows = 2;         // slot rows per thread (1 or 2)
+    bool mut = true;      // mu rides in the ring slots (TMA); else per-thread loads from L2
     int TY = 0, ntiles = 0, nslots = 0, threads = 512;
     size_t smem = 0;
 };
 // prefetch: planes loaded ahead (1..3; slots = prefetch + 2); want_ty > 0 forces the tile height,
 // want_rows > 0 the rows per thread
-CgTiling cg_tiling(int nx, int ny, int nz, int prefetch = 2, int want_ty = 0, int want_rows = 0);
-size_t pass_smem(int nx, int TY, int NS, int nz);
+CgTiling cg_tiling(int nx, int ny, int nz, int prefetch = 2, int want_ty = 0, int want_rows = 0, bool no_mu = false);
+size_t pass_smem(int nx, int TY, int NS, int nz, bool mut);
 
 struct PassArgs {
     OpConst op;
