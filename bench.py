@@ -4,16 +4,19 @@
 One step at 64^3, 256 sources x 256 detectors x 3
 frequencies, 16 RBFs (80 parameters):
   set_params(p)            PaLS mu(x,p), support S of dA/dp, G on S
-  jacobian(I, I)           all 256 forward + 256 adjoint RHS per frequency
-                           (1536 COCG solves) and the full Jacobian on FP64 DMMA
+  jacobian(I, I)           all 256 forward + 256 adjoint RHS per frequency (1536 systems,
+                           solved as 512 real multi-shift CG seeds) and the full Jacobian
+                           on FP64 DMMA
   misfit(I, I)             full-data misfit from the cached forward fields
   jacobian(W, V)           sketched Jacobian, W, V Rademacher 256 x 12
-Metric: RHS solves/s (whole job), with the COCG pass kernel's HBM roofline and
-the Jacobian contraction's FP64 TFLOP/s reported beside it.
+Metric: RHS solves/s (whole job; one solve = one (right-hand side, frequency) system), with
+the CG pass kernel's HBM roofline and the Jacobian contraction's FP64 TFLOP/s beside it.
+--config sketch32 | opt96 | all128 runs the other BASELINE rows (all128: configs[4], the
+all-sources step with the full Jacobian).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-Multi-GPU: launched by torch.distributed.run; RHS columns are sharded across
-ranks (paper_1706_05586_b200/sharded.py), rank 0 prints one JSON line.
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
+Multi-GPU: launched by torch.distributed.run; RHS columns are sharded across ranks
+(full64, all128; paper_1706_05586_b200/sharded.py), rank 0 prints one JSON line.
 """
 from __future__ import annotations
 
@@ -442,7 +445,9 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f64",
+        "dtype_note": "fp64 throughout: real seed CG in f64, complex (c128) shifted recurrences, fields and J",
+        "data": "synthetic",
         "config": {"workload": cfg.name, "grid": list(cfg.n), "sources": cfg.n_s, "detectors": cfg.n_d,
                    "frequencies": cfg.n_freq, "n_params": cfg.n_p, "sketch": [cfg.ls, cfg.ld],
                    "solves_per_step": solves_per_step, "parallelism": f"rhs-shard x{world}",
