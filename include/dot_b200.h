@@ -204,8 +204,9 @@ int dot_optimize_directions_subspace(dot_problem* P, int32_t k, int32_t iters, i
  * dot_nccl_unique_id: 128-byte NCCL id (host); rank 0 creates it, the caller
  *   broadcasts it (e.g. torch.distributed).  NCCL is loaded at run time.
  * dot_dd_create: `local` [nlocal] problems of ranks rank0 .. rank0+nlocal-1.  Either
- *   nlocal == world or nlocal == 1 with nccl_id.  All ranks hold the same problem and
- *   parameters (dot_set_params on each).
+ *   nlocal == world (in-process) or nlocal == 1 with nccl_id (one rank per process; world 1
+ *   with an id runs the NCCL path on one GPU: all-reduces, no neighbours).  All ranks hold
+ *   the same problem and parameters (dot_set_params on each).
  * dot_transport: sendrecv(ctx, peer, send, send_bytes, recv, recv_bytes) exchanges host
  *   buffers with rank `peer` (the peer calls it with the mirrored sizes; either size may be
  *   0); allreduce_sum(ctx, buf, n) sums n doubles in place over all ranks.  Both return 0

@@ -779,7 +779,7 @@ void dd_solve(dot_dd* G, const std::vector<Req>& reqs) {
     const int nb = sp.nseeds / 2, ns = sp.nseeds;
     const DDPlan pl = dd_plan(G, nb);
     const int ntiles = P0->tl.ntiles, nslots = ntiles * pl.C;
-    const bool local = (L == G->world);
+    const bool local = (L == G->world) && !G->comm && !G->host;
     std::unique_ptr<Transport> tr;
     if (!local) {
         if (G->comm) tr.reset(new NcclTransport(G->comm, G->rank0));
@@ -1685,7 +1685,7 @@ int dot_dd_create(dot_problem* const* local, int32_t nlocal, int32_t rank0, int3
         }
         G->rank0 = rank0;
         G->world = world;
-        if (nlocal < world) {
+        if (nlocal < world || (nccl_id && world == 1)) {   // one rank per process (world 1: NCCL smoke)
             if (!nccl_id) throw Error(DOT_ERR_ARG, "multi-process decomposition needs an NCCL unique id");
             NcclApi& nc = nccl_api();
             if (!nc.ok) throw Error(DOT_ERR_CUDA, nc.why);

@@ -175,3 +175,25 @@ def test_transport_dd_multiprocess_gloo_matches_oracle(dot, ci, world):
         assert abs(m - m_or) <= 1e-8 * m_or, (rank, m, m_or)
         assert rel(J, J_or) <= 1e-7, rank
     assert abs(res[0][2] - res[world - 1][2]) <= 1e-12 * res[0][2]
+
+
+def test_nccl_transport_single_rank_matches_oracle(dot):
+    """The NCCL transport of dd_solve on one GPU (world 1: ncclCommInitRank, the all-reduces of
+    the Krylov partials and of the sampled solutions through NCCL; no halo neighbours) gives
+    the oracle's misfit and Jacobian.  The multi-rank send/recv needs several GPUs."""
+    from paper_1706_05586_b200.dd import _DD, nccl_unique_id
+    cfg = small_config(**CASES[0], eps=0.4)
+    prob, wl = small_problem(cfg, with_data=True)
+    rng = np.random.default_rng(5)
+    W = np.sign(rng.standard_normal((cfg.n_s, 3)))
+    V = np.sign(rng.standard_normal((cfg.n_d, 2)))
+    g = dot.DOTProblem.from_config(cfg, wl.src_nodes, wl.det_nodes)
+    g.set_data(prob.data)
+    g.set_params(wl.p)
+    dd = _DD([g], 0, 1, nccl_id=nccl_unique_id())
+    dd.fields(W, V)
+    m, J = g.misfit(W, V), g.jacobian(W, V)
+    m_or, J_or = misfit(prob, wl.p, W, V), jacobian(prob, wl.p, W, V)
+    assert abs(m - m_or) <= 1e-8 * m_or
+    assert rel(J, J_or) <= 1e-7
+    dd.close()
