@@ -59,7 +59,11 @@ def selection(n, lo, hi):
 
 def make_problem_for_rank(dot, cfg, wl, plan, **kw):
     """Every rank holds the full problem description (all sources/detectors);
-    the shard decides which RHS it solves."""
+    the shard decides which RHS it solves.  The workspace is sized for this rank's share of
+    the systems (n_freq x (its source + detector columns)), leaving device memory for the
+    gathered fields and Jacobian blocks."""
+    if plan.world > 1 and "max_rhs" not in kw and "workspace_bytes" not in kw:
+        kw["max_rhs"] = cfg.n_freq * (plan.per_src + plan.per_det)
     return dot.DOTProblem.from_config(cfg, wl.src_nodes, wl.det_nodes, **kw)
 
 
@@ -163,15 +167,24 @@ def sharded_step(backend, plan: ShardPlan, p, W, V, data=None, device=None, comm
     tdist.all_gather([torch.view_as_real(t) for t in parts], torch.view_as_real(pad))
     U_all = torch.cat([parts[r][:, : plan.src_block(r)[1] - plan.src_block(r)[0]] for r in range(plan.world)], 1)
     J_rows = T(backend.contract(L_blk, U_all.to(dev), G)) if dhi > dlo else None   # [nf][nd_r][ns][np]
-    rows = torch.zeros((nf, plan.per_det, plan.n_s, G.shape[1]), dtype=torch.complex128, device=cdev)
-    if J_rows is not None:
-        rows[:, : J_rows.shape[1]] = J_rows.to(cdev)
-    gathered = [torch.empty_like(rows) for _ in range(plan.world)] if plan.rank == 0 else None
-    tdist.gather(torch.view_as_real(rows), [torch.view_as_real(t) for t in gathered] if gathered else None, dst=0)
+    # J blocks to rank 0, one rank at a time into the final array (peak: J + one block)
     J_full = None
+    n_p = G.shape[1]
     if plan.rank == 0:
-        J_full = torch.cat([gathered[r][:, : plan.det_block(r)[1] - plan.det_block(r)[0]]
-                            for r in range(plan.world)], 1)
+        J_full = torch.empty((nf, plan.n_d, plan.n_s, n_p), dtype=torch.complex128, device=cdev)
+        if J_rows is not None:
+            J_full[:, dlo:dhi] = J_rows.to(cdev)
+        tmp = torch.empty(nf * plan.per_det * plan.n_s * n_p, dtype=torch.complex128, device=cdev)
+        for r in range(1, plan.world):
+            lo, hi = plan.det_block(r)
+            if hi <= lo:
+                continue
+            blk = tmp[: nf * (hi - lo) * plan.n_s * n_p].view(nf, hi - lo, plan.n_s, n_p)   # contiguous
+            tdist.recv(torch.view_as_real(blk), src=r)
+            J_full[:, lo:hi] = blk
+        del tmp
+    elif J_rows is not None:
+        tdist.send(torch.view_as_real(J_rows.to(cdev).contiguous()), dst=0)
     d2h = 0
     if host_io:
         d2h += 8
