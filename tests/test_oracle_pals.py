@@ -66,6 +66,25 @@ def test_absorption_range_and_midpoint():
     assert (mu > cfg.mua_bg).any()
 
 
+def test_absorption_orientation_and_midpoint():
+    """Eq. (2.4) / PAPER.md L153-155: mu = mu_in where phi - c > eps (inside the anomaly),
+    mu_out where phi - c < -eps, and (mu_in + mu_out)/2 where phi = c exactly (H_eps(0) = 1/2).
+    One basis centred on a node with alpha chosen so that phi(node) = c: the node sits on the
+    level set; nodes beyond the basis's support read mu_out."""
+    cfg = config_by_name("tiny16")
+    g = make_grid(cfg.n, cfg.L)
+    node = 5 * 16 * 16 + 7 * 16 + 6
+    chi = (g.X[node], g.Y[node], g.Z[node])
+    beta = 1.0
+    alpha_mid = cfg.cutoff / wendland(cfg.gamma)           # phi(node) = alpha psi(gamma) = c
+    mu = absorption(np.array([alpha_mid, beta, *chi]), g, cfg)
+    assert mu[node] == pytest.approx(0.5 * (cfg.mua_anom + cfg.mua_bg), rel=1e-12)
+    far = np.sqrt((g.X - chi[0]) ** 2 + (g.Y - chi[1]) ** 2 + (g.Z - chi[2]) ** 2) > 1.0 / beta
+    assert np.all(mu[far] == cfg.mua_bg)                     # outside: mu_out
+    mu_in = absorption(np.array([1.0, beta, *chi]), g, cfg)  # phi(node) = psi(gamma) ~ 1 >> c + eps
+    assert mu_in[node] == cfg.mua_anom                       # inside: mu_in (orientation)
+
+
 @pytest.mark.parametrize("seed", [0, 1, 2])
 def test_dmu_dp_matches_central_differences(seed):
     cfg = config_by_name("tiny16").with_(eps=0.4, n=(10, 10, 10))
