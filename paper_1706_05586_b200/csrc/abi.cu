@@ -235,7 +235,7 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, c
     const int chunk = (int)std::min<size_t>(fit, (size_t)npairs);
     const int CHK = 8;
     // z chunks: enough CTAs to fill the GPU when few pairs iterate together on a deep grid
-    // (DESIGN.md "z chunks"); at least 8 planes per chunk.  DOT_CG_ZCHUNKS overrides.
+    // (DESIGN.md "z chunks"); at least 4 planes per chunk.  DOT_CG_ZCHUNKS overrides.
     auto zchunks = [&](int nb) {
         int n = 1;
         const char* e = std::getenv("DOT_CG_ZCHUNKS");
@@ -243,11 +243,12 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, c
             n = std::min(std::max(1, std::atoi(e)), std::max(1, P->nz / 4));
         } else {
             // wave model: a pass costs ~ ceil(CTAs / SMs) waves x (planes per chunk + 4 halo planes +
-            // ~2 planes of start-up); pick the chunk count that minimises it (chunks >= 8 planes).
+            // ~2 planes of start-up); pick the chunk count that minimises it.  sketch32 at 8 pairs:
+            // 4 / 8 chunks 0.13 / 0.17 of the HBM peak (latency-bound: one wave of 16-64 CTAs).
             // Measured (tools/pass_bench.py): opt96 at 12 pairs 0.41 / 0.51 / 0.47 of the HBM peak with
             // 1 / 2 / 4 chunks -- the model's choice is 2.
             const long long have = (long long)P->tl.ntiles * nb;
-            const int nmax = std::max(1, P->nz / 8);
+            const int nmax = std::max(1, P->nz / 4);           // chunks of >= 4 planes
             double best = 0;
             for (int c = 1; c <= nmax; ++c) {
                 const long long waves = (have * c + P->num_sms - 1) / P->num_sms;
