@@ -60,6 +60,7 @@ struct dot_problem {
     DBuf<int32_t> d_seg, d_segoff;    // block sparsity of G by basis (GSparse)
     DBuf<int32_t> d_segslot;          // [T] sample slot of the basis-ordered support points
     DBuf<double> d_Gseg;              // [T][5] basis-ordered weights
+    DBuf<int32_t> d_ktile, d_kto;     // k-tiles of the segment GEMM (GSparse::ktile, ::kto)
     GSparse gsp;
     DBuf<double2> d_Dt;               // data, [n_freq][n_src][n_det]
     FieldCache cache[2];              // 0: sources, 1: detectors
@@ -1165,6 +1166,8 @@ size_t dot_workspace_bytes(const dot_problem* P, int32_t max_rhs) {
     // the Jacobian's support panels / combined fields, and the host-staged full Jacobian
     fixed += 2 * (size_t)P->n_freq * (P->n_src + P->n_det) * Kb * sizeof(double2);
     fixed += (size_t)P->n_freq * P->n_src * P->n_det * std::max(P->n_p, 1) * sizeof(double2);
+    // one frequency's operand tiles of the segment GEMM (every support point in every basis)
+    fixed += contract_seg_tma_bytes(P->n_det, P->n_src, (long long)Kb * 2, P->n_rbf);
     // max_rhs systems = max_rhs / n_freq real seeds (all shifts of one seed together), in pairs
     const size_t pairs = ((size_t)std::max(max_rhs, 1) + 2 * P->n_freq - 1) / (2 * P->n_freq) + 1;
     // dense solutions (dot_solve: every node sampled) of up to 3 complex right-hand sides
@@ -1276,6 +1279,8 @@ int dot_set_params(dot_problem* P, const double* p, int where) {
     P->d_segoff.reset();
     P->d_segslot.reset();
     P->d_Gseg.reset();
+    P->d_ktile.reset();
+    P->d_kto.reset();
     P->gsp = GSparse{};
     launch_compact(P->d_flagS.get(), P->d_posS.get(), N, P->d_S.get(), s);
     launch_compact(P->d_flagP.get(), P->d_posP.get(), N, P->d_P.get(), s);
@@ -1297,9 +1302,25 @@ int dot_set_params(dot_problem* P, const double* p, int where) {
             P->d_segoff = DBuf<int32_t>(P->arena, P->n_rbf + 1);
             launch_rbf_segments(F.get(), Fpos.get(), P->K, P->n_rbf, P->d_tot.get() + 2, P->d_seg.get(),
                                 P->d_segoff.get(), s);
+            std::vector<int32_t> hoff(P->n_rbf + 1);
+            DOT_CUDA_TRY(cudaMemcpyAsync(hoff.data(), P->d_segoff.get(), hoff.size() * sizeof(int32_t),
+                                         cudaMemcpyDeviceToHost, s));
             P->stats.kernel_launches += 5;
             sync(P);
-            P->gsp = GSparse{P->d_seg.get(), P->d_segoff.get(), P->n_rbf, T};
+            // k-tiles of 16 points per basis (the segment GEMM's blocks never straddle bases)
+            std::vector<int32_t> kto(P->n_rbf + 1, 0), ktile;
+            for (int j = 0; j < P->n_rbf; ++j) {
+                kto[j + 1] = kto[j] + (hoff[j + 1] - hoff[j] + 15) / 16;
+                for (int t = hoff[j]; t < hoff[j + 1]; t += 16) {
+                    ktile.push_back(t);
+                    ktile.push_back(hoff[j + 1]);
+                }
+            }
+            if (ktile.empty()) ktile.assign(2, 0);
+            P->d_kto = to_device(P, kto.data(), kto.size(), DOT_HOST);
+            P->d_ktile = to_device(P, ktile.data(), ktile.size(), DOT_HOST);
+            P->gsp = GSparse{P->d_seg.get(), P->d_segoff.get(), P->n_rbf, T,
+                             reinterpret_cast<const int2*>(P->d_ktile.get()), P->d_kto.get(), kto[P->n_rbf]};
             P->d_segslot = DBuf<int32_t>(P->arena, std::max(T, 1));
             P->d_Gseg = DBuf<double>(P->arena, 5 * (size_t)std::max(T, 1));
             launch_compose_index(P->d_seg.get(), T, P->d_S_slot.get(), P->d_segslot.get(), s);
@@ -1360,6 +1381,19 @@ int dot_misfit(dot_problem* P, const double* W, int32_t ls, const double* V, int
     DOT_API_END(P)
 }
 
+// block-sparse segment GEMM of basis-ordered panels (DOT_SEG_V1: the round-2a kernel, A/B only)
+static void contract_seg(dot_problem* P, int nf, int T, int ld, int ls, const double2* L, size_t lbs, const double2* U,
+                         size_t ubs, double2* J) {
+    static const bool v1 = std::getenv("DOT_SEG_V1") != nullptr;
+    if (v1) {
+        launch_contract_seg(nf, T, ld, ls, P->n_p, P->n_rbf, L, lbs, U, ubs, P->d_Gseg.get(), P->gsp.segoff, J,
+                            P->stream);
+        return;
+    }
+    contract_seg_tma(nf, T, ld, ls, P->n_p, L, lbs, U, ubs, P->d_Gseg.get(), P->gsp, J, P->arena, P->stream,
+                     &P->stats.kernel_launches);
+}
+
 int dot_jacobian(dot_problem* P, const double* W, int32_t ls, const double* V, int32_t ld, int where,
                  double* J_out) {
     DOT_API_BEGIN
@@ -1396,8 +1430,7 @@ int dot_jacobian(dot_problem* P, const double* W, int32_t ls, const double* V, i
         DOT_CUDA_TRY(cudaEventRecord(e0, s));
     }
     if (seg)
-        launch_contract_seg(nf, Kp, ld, ls, P->n_p, P->n_rbf, LS.get(), (size_t)ld * Kp, US.get(), (size_t)ls * Kp,
-                            P->d_Gseg.get(), P->gsp.segoff, J, s);
+        contract_seg(P, nf, Kp, ld, ls, LS.get(), (size_t)ld * Kp, US.get(), (size_t)ls * Kp, J);
     else
         launch_contract(nf, K, ld, ls, P->n_p, LS.get(), (size_t)ld * K, US.get(), (size_t)ls * K, P->d_G.get(), J, s,
                         &P->gsp);
@@ -1769,11 +1802,13 @@ int dot_contract_fields(dot_problem* P, int32_t ld, int32_t ls, const double* La
     const int nf = P->n_freq, K = P->K;
     cudaStream_t s = P->stream;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (P->timing) {
-        e0 = event_at(P, 0);
-        e1 = event_at(P, 1);
-        DOT_CUDA_TRY(cudaEventRecord(e0, s));
-    }
+    auto start_timer = [&]() {                 // brackets the contraction kernel only
+        if (P->timing) {
+            e0 = event_at(P, 0);
+            e1 = event_at(P, 1);
+            DOT_CUDA_TRY(cudaEventRecord(e0, s));
+        }
+    };
     if (contract_seg_applies(ld, ls, &P->gsp, P->n_p)) {
         // reorder the S-ordered panels into basis order (one gather), then the segment GEMM
         const int T = (int)P->gsp.total;
@@ -1782,10 +1817,11 @@ int dot_contract_fields(dot_problem* P, int32_t ld, int32_t ls, const double* La
                            (size_t)ld * T, T, s);
         launch_gather_cols(nf, ls, T, reinterpret_cast<const double2*>(U), (size_t)ls * K, K, P->gsp.seg, Ug.get(),
                            (size_t)ls * T, T, s);
-        launch_contract_seg(nf, T, ld, ls, P->n_p, P->n_rbf, Lg.get(), (size_t)ld * T, Ug.get(), (size_t)ls * T,
-                            P->d_Gseg.get(), P->gsp.segoff, reinterpret_cast<double2*>(J), s);
+        start_timer();
+        contract_seg(P, nf, T, ld, ls, Lg.get(), (size_t)ld * T, Ug.get(), (size_t)ls * T, reinterpret_cast<double2*>(J));
         P->stats.kernel_launches += 3;
     } else {
+        start_timer();
         launch_contract(nf, K, ld, ls, P->n_p, reinterpret_cast<const double2*>(Lam), (size_t)ld * K,
                         reinterpret_cast<const double2*>(U), (size_t)ls * K, P->d_G.get(), reinterpret_cast<double2*>(J),
                         s, &P->gsp);

@@ -11,6 +11,7 @@
 // double-buffered in shared memory: the global loads of k-tile t+1 are issued
 // into registers before the DMMAs of tile t and land in the other buffer after
 // them -- one barrier per k-tile.  8 warps, warp w owns rows 16w .. 16w+15.
+#include "arena.h"
 #include "kernels.h"
 
 namespace dot {
@@ -274,12 +275,18 @@ __global__ void __launch_bounds__(THREADS) contract_sparse_kernel(int K, int ld,
 //     P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi);  re = P1 - P2, im = P3 - P1 - P2
 // (3 DMMA per fragment instead of 4).  B = Gs * U is formed in the fragment load.
 // Warp w: rows 16 (w & 3) .. +16, columns 32 (w >> 2) .. +32.
-constexpr int QM = 64, QN = 64, QK = 16, QRS = QK + 1, QST = 3;   // QRS: padded row stride (double2)
+// QRS: padded row stride in double2; QRS = 4 (mod 8) makes every 8-lane phase of a fragment
+// load (2 rows x 4 k) hit 8 distinct 16-byte bank groups (conflict-free LDS.128).
+constexpr int QM = 64, QN = 64, QK = 16, QRS = QK + 4, QST = 3;
 constexpr size_t kSegStage = (size_t)(QM + QN) * QRS * sizeof(double2) + QK * 5 * sizeof(double);
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
     const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
 }
 
 __global__ void __launch_bounds__(THREADS, 1) contract_seg_kernel(int T, int ld, int ls, int n_rbf,
@@ -324,10 +331,9 @@ __global__ void __launch_bounds__(THREADS, 1) contract_seg_kernel(int T, int ld,
             cp_async16(stA(st) + row * QRS + kk, kin && aok[e] ? asrc[e] + k0 : Lf, kin && aok[e]);
             cp_async16(stU(st) + row * QRS + kk, kin && uok[e] ? usrc[e] + k0 : Uf, kin && uok[e]);
         }
-        if (threadIdx.x < QK * 5) {
-            const int kk = threadIdx.x / 5, q = threadIdx.x % 5;
-            const int t = s0 + k0 + kk;
-            stG(st)[kk * 5 + q] = t < s1 ? Gs[(size_t)t * 5 + q] : 0.0;
+        if (threadIdx.x < QK * 5) {            // the weights ride in the same async group (no
+            const int t = s0 + k0 + threadIdx.x / 5;    // synchronous global load per k-tile)
+            cp_async8(stG(st) + threadIdx.x, t < s1 ? Gs + (size_t)s0 * 5 + k0 * 5 + threadIdx.x : Gs, t < s1);
         }
     };
     // per-thread fragment columns: n = wn + ni*8 + lane/4 -> parameter q of that column
@@ -400,6 +406,178 @@ __global__ void __launch_bounds__(THREADS, 1) contract_seg_kernel(int T, int ld,
                 const double re = p1[mi][ni][h] - p2[mi][ni][h];
                 const double im = p3[mi][ni][h] - p1[mi][ni][h] - p2[mi][ni][h];
                 J[((size_t)f * npairs + (size_t)d * ls + i) * n_p + 5 * jb + q] = make_double2(-re, -im);
+            }
+    }
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// ------------------------------------- segment GEMM on pre-formed operand tiles (default)
+// J[d][(q, i)] = - sum_{t in basis j} Lam[d][t] (Gs[t][q] U[i][t]) as the 3-multiply complex
+// GEMM of seg_v1 above, with every FP64 ALU operation moved out of the DMMA loop: on sm_100
+// DADD / DMUL issue into the FP64 pipe DMMA uses (ncu: math-pipe stalls on DADD beside DMMA,
+// DMMA pipe 56-70 % with them in the loop, 100 % without, tools/dmma_probe.cu).
+//  * seg_prescale_kernel writes, per frequency, the operands as blocks of 64 rows x 16
+//    points (a k-tile never straddles two bases; zero rows / points pad the tails) laid out
+//    exactly as the GEMM's shared stage: [64][16] double2 (re, im) then [64][16] double
+//    (re + im), the point index XOR-swizzled per row so fragment loads are conflict-free
+//    (double2: kk ^ 4 (row & 1); double: kk ^ 4 (row & 3)).  A rows are detectors (Lam),
+//    B rows are (q, i) = q ls + i with the weight folded in (Gs[t][q] U[i][t]).
+//  * seg_tma_gemm_kernel: one producer lane streams the A and B block of each k-tile with one
+//    cp.async.bulk each into a 4-stage ring (full / empty mbarriers); 8 consumer warps (2 per
+//    scheduler), warp tile 16 x 32, run LDS + DMMA only (3 DMMA per fragment pair).
+namespace tma {
+constexpr int QM = 64, KT = 16, BLK = QM * KT * 24, NST = 4, NCW = 8, NT = 32 * (NCW + 1);
+constexpr size_t SMEM = 128 + (size_t)NST * 2 * BLK;
+static_assert(SMEM <= 232448, "seg_tma_gemm shared memory");
+}  // namespace tma
+
+template <int SIDE>
+__global__ void __launch_bounds__(256) seg_prescale_kernel(int rows, int ls, int T, const double2* __restrict__ P,
+                                                           const double* __restrict__ Gs,
+                                                           const int2* __restrict__ ktile, int KTn, int rt0,
+                                                           unsigned char* out) {
+    const int g = blockIdx.x, rt = rt0 + blockIdx.y;
+    unsigned char* base = out + ((size_t)blockIdx.y * KTn + g) * tma::BLK;
+    double2* o2 = reinterpret_cast<double2*>(base);
+    double* o1 = reinterpret_cast<double*>(base + tma::QM * tma::KT * 16);
+    const int2 kt = ktile[g];
+    for (int e = threadIdx.x; e < tma::QM * tma::KT; e += blockDim.x) {
+        const int r = e >> 4, kk = e & 15, n = rt * tma::QM + r, t = kt.x + kk;
+        double2 v = make_double2(0.0, 0.0);
+        double sm = 0.0;
+        if (n < rows && t < kt.y) {
+            if (SIDE == 0) {
+                v = P[(size_t)n * T + t];
+                sm = v.x + v.y;
+            } else {
+                const int q = n / ls, i = n - q * ls;
+                const double2 u = P[(size_t)i * T + t];
+                const double w = Gs[(size_t)t * 5 + q];
+                v = make_double2(w * u.x, w * u.y);
+                sm = w * (u.x + u.y);
+            }
+        }
+        o2[r * 16 + (kk ^ ((r & 1) << 2))] = v;
+        o1[r * 16 + (kk ^ ((r & 3) << 2))] = sm;
+    }
+}
+
+__global__ void __launch_bounds__(tma::NT, 1) seg_tma_gemm_kernel(int ld, int ls, int n_p, const unsigned char* Ap,
+                                                                 const unsigned char* Bp, int KTn,
+                                                                 const int32_t* __restrict__ kto, int nt0,
+                                                                 double2* J) {
+    using tma::KT;
+    using tma::NST;
+    using tma::NCW;
+    using tma::BLK;
+    constexpr int TM = tma::QM;
+    extern __shared__ __align__(128) unsigned char tsm[];
+    const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(tsm));   // full[NST], empty[NST]
+    const uint32_t st0 = bar0 + 128;
+    const int dt = blockIdx.x, ntl = blockIdx.y, j = blockIdx.z;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g0 = kto[j], nkt = kto[j + 1] - g0;
+    if (tid == 0) {
+        for (int s = 0; s < NST; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar0 + 8 * s), "r"(1));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar0 + 8 * (NST + s)), "r"(32 * NCW));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == NCW) {                                   // producer: one lane streams the blocks
+        if (lane == 0) {
+            const unsigned char* a = Ap + ((size_t)dt * KTn + g0) * BLK;
+            const unsigned char* b = Bp + ((size_t)ntl * KTn + g0) * BLK;
+            for (int t = 0; t < nkt; ++t) {
+                const int s = t % NST;
+                if (t >= NST) mbar_wait(bar0 + 8 * (NST + s), ((t / NST) - 1) & 1);
+                const uint32_t fb = bar0 + 8 * s, dA = st0 + s * 2 * BLK;
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(2 * BLK)
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dA),
+                    "l"(a + (size_t)t * BLK), "r"(BLK), "r"(fb)
+                    : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        dA + BLK),
+                    "l"(b + (size_t)t * BLK), "r"(BLK), "r"(fb)
+                    : "memory");
+            }
+        }
+        return;
+    }
+    const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;
+    const int r4 = lane >> 2, sw2 = (r4 & 1) << 2, sw1 = (r4 & 3) << 2;
+    double p1[2][4][2], p2[2][4][2], p3[2][4][2];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) p1[mi][ni][h] = p2[mi][ni][h] = p3[mi][ni][h] = 0.0;
+    for (int t = 0; t < nkt; ++t) {
+        const int s = t % NST;
+        mbar_wait(bar0 + 8 * s, (t / NST) & 1);
+        const unsigned char* sa = tsm + 128 + (size_t)s * 2 * BLK;
+        const double2* A2 = reinterpret_cast<const double2*>(sa);
+        const double* A1 = reinterpret_cast<const double*>(sa + TM * KT * 16);
+        const double2* B2 = reinterpret_cast<const double2*>(sa + BLK);
+        const double* B1 = reinterpret_cast<const double*>(sa + BLK + TM * KT * 16);
+#pragma unroll
+        for (int k4 = 0; k4 < KT; k4 += 4) {
+            const int kk = k4 + (lane & 3);
+            double2 a[2];
+            double as[2];
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi) {
+                const int r = wm + mi * 8 + r4;
+                a[mi] = A2[r * 16 + (kk ^ sw2)];
+                as[mi] = A1[r * 16 + (kk ^ sw1)];
+            }
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+                const int r = wn + ni * 8 + r4;
+                const double2 b = B2[r * 16 + (kk ^ sw2)];
+                const double bs = B1[r * 16 + (kk ^ sw1)];
+#pragma unroll
+                for (int mi = 0; mi < 2; ++mi) {
+                    dmma(p1[mi][ni][0], p1[mi][ni][1], a[mi].x, b.x);
+                    dmma(p2[mi][ni][0], p2[mi][ni][1], a[mi].y, b.y);
+                    dmma(p3[mi][ni][0], p3[mi][ni][1], as[mi], bs);
+                }
+            }
+        }
+        mbar_arrive(bar0 + 8 * (NST + s));
+    }
+    // epilogue: J[(d, i)][5 j + q] = -C[d][q ls + i]
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+        const int d = dt * TM + wm + mi * 8 + r4;
+        if (d >= ld) continue;
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int n = (nt0 + ntl) * TM + wn + ni * 8 + 2 * (lane & 3) + h;
+                if (n >= 5 * ls) continue;
+                const int q = n / ls, i = n - q * ls;
+                const double re = p1[mi][ni][h] - p2[mi][ni][h];
+                const double im = p3[mi][ni][h] - p1[mi][ni][h] - p2[mi][ni][h];
+                J[((size_t)d * ls + i) * n_p + 5 * j + q] = make_double2(-re, -im);
             }
     }
 }
@@ -484,6 +662,48 @@ void launch_compose_index(const int32_t* seg, int T, const int32_t* slot, int32_
     if (T <= 0) return;
     compose_index_kernel<<<(unsigned)std::min(1024, (T + 255) / 256), 256, 0, s>>>(seg, T, slot, idx);
     DOT_CUDA_TRY(cudaGetLastError());
+}
+
+size_t contract_seg_tma_bytes(int ld, int ls, long long total, int n_rbf) {
+    const size_t kts = (size_t)(total + tma::KT - 1) / tma::KT + n_rbf;
+    return ((size_t)(ld + tma::QM - 1) / tma::QM + (5 * (size_t)ls + tma::QM - 1) / tma::QM) * kts * tma::BLK;
+}
+
+void contract_seg_tma(int nb, int T, int ld, int ls, int n_p, const double2* Lam, size_t lam_bstride,
+                      const double2* U, size_t u_bstride, const double* Gs, const GSparse& sp, double2* J,
+                      Arena& arena, cudaStream_t s, int64_t* launches) {
+    if (nb <= 0 || ld <= 0 || ls <= 0) return;
+    const int npairs = ld * ls;
+    if (T <= 0 || sp.ktiles <= 0) {
+        DOT_CUDA_TRY(cudaMemsetAsync(J, 0, (size_t)nb * npairs * n_p * sizeof(double2), s));
+        return;
+    }
+    const int KTn = sp.ktiles;
+    const int nDT = (ld + tma::QM - 1) / tma::QM, nNT = (5 * ls + tma::QM - 1) / tma::QM;
+    const size_t per_tile = (size_t)KTn * tma::BLK;
+    DBuf<unsigned char> Ap(arena, nDT * per_tile);
+    // B operand tiles: all column tiles of a frequency if the workspace holds them, else chunks
+    const size_t room = arena.largest_free();
+    int chunk = (int)std::max<size_t>(1, std::min<size_t>(nNT, room > per_tile ? room / per_tile : 1));
+    if (const char* e = std::getenv("DOT_SEG_CHUNK")) chunk = std::max(1, std::min(chunk, std::atoi(e)));  // tests
+    DBuf<unsigned char> Bp(arena, (size_t)chunk * per_tile);
+    ensure_smem(seg_tma_gemm_kernel, tma::SMEM);
+    for (int f = 0; f < nb; ++f) {
+        seg_prescale_kernel<0><<<dim3(KTn, nDT), 256, 0, s>>>(ld, ls, T, Lam + (size_t)f * lam_bstride, Gs, sp.ktile, KTn,
+                                                             0, Ap.get());
+        DOT_CUDA_TRY(cudaGetLastError());
+        *launches += 1;
+        for (int nt0 = 0; nt0 < nNT; nt0 += chunk) {
+            const int nn = std::min(chunk, nNT - nt0);
+            seg_prescale_kernel<1><<<dim3(KTn, nn), 256, 0, s>>>(5 * ls, ls, T, U + (size_t)f * u_bstride, Gs,
+                                                                sp.ktile, KTn, nt0, Bp.get());
+            DOT_CUDA_TRY(cudaGetLastError());
+            seg_tma_gemm_kernel<<<dim3(nDT, nn, sp.n_rbf), tma::NT, tma::SMEM, s>>>(
+                ld, ls, n_p, Ap.get(), Bp.get(), KTn, sp.kto, nt0, J + (size_t)f * npairs * n_p);
+            DOT_CUDA_TRY(cudaGetLastError());
+            *launches += 2;
+        }
+    }
 }
 
 void launch_contract(int nb, int K, int ld, int ls, int n_p, const double2* Lam, size_t lam_bstride,

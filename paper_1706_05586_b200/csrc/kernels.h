@@ -5,6 +5,8 @@
 
 namespace dot {
 
+class Arena;
+
 // ------------------------------------------------------------------ cg_shift.cu
 // Tiling of the fused multi-shift CG pass: a CTA owns TY full x-rows of one pair of real
 // seeds and marches the nz planes; planes (with a 2-row y halo) are staged by TMA bulk
@@ -121,6 +123,11 @@ struct GSparse {
     const int32_t* segoff = nullptr;   // [n_rbf + 1]
     int n_rbf = 0;
     long long total = 0;               // segoff[n_rbf]
+    // k-tiles of 16 basis-ordered points that never straddle two bases (contract_seg_tma):
+    // ktile[g] = (first point, end of its basis's points), kto[j] = first k-tile of basis j
+    const int2* ktile = nullptr;
+    const int32_t* kto = nullptr;      // [n_rbf + 1]
+    int ktiles = 0;                    // kto[n_rbf]
 };
 // sp == null (or no segments): dense DMMA contraction over all K points; else the
 // block-sparse one (per basis j, its support points only).
@@ -134,6 +141,17 @@ bool contract_seg_applies(int ld, int ls, const GSparse* sp, int n_p);
 void launch_contract_seg(int nb, int T, int ld, int ls, int n_p, int n_rbf, const double2* Lam, size_t lam_bstride,
                          const double2* U, size_t u_bstride, const double* Gs, const int32_t* segoff, double2* J,
                          cudaStream_t s);
+// The same GEMM through pre-formed operand tiles (default): per frequency, a prescale pass
+// writes the 3-multiply operands (A = Lam, B = Gs U as (re, im) + (re + im) planes) as
+// 64-row x 16-point blocks in the exact shared-memory image the GEMM consumes; the GEMM
+// streams them with one cp.async.bulk per block into a 4-stage mbarrier ring and runs LDS +
+// DMMA only.  Operand tiles come from `arena` (chunked over column tiles when it is short);
+// launches are added to *launches.
+void contract_seg_tma(int nb, int T, int ld, int ls, int n_p, const double2* Lam, size_t lam_bstride,
+                      const double2* U, size_t u_bstride, const double* Gs, const GSparse& sp, double2* J,
+                      Arena& arena, cudaStream_t s, int64_t* launches);
+// bytes of one frequency's operand tiles (the workspace estimate)
+size_t contract_seg_tma_bytes(int ld, int ls, long long total, int n_rbf);
 // Gs[t][q] = G[seg[t]][5 j + q]
 void launch_seg_weights(const double* G, int n_p, const GSparse& sp, double* Gs, cudaStream_t s);
 // idx[t] = slot[seg[t]]

@@ -437,3 +437,26 @@ def test_block_sparse_gemm_contraction_equals_dense(dot, monkeypatch):
     assert rel(Js, Jd) < 1e-12
     Jo = jacobian(prob, wl.p, np.eye(cfg.n_s), np.eye(cfg.n_d))
     assert rel(Js, Jo) < 1e-7
+
+
+@pytest.mark.parametrize("chunk", [None, "1"])
+def test_segment_gemm_ragged_tiles_and_chunks(dot, monkeypatch, chunk):
+    """The pre-formed-operand segment GEMM over several 64-row tiles on both sides with
+    ragged tails (ld = 70 detectors, 5 ls = 65 (q, i) rows), bases whose point counts are
+    not multiples of the 16-point k-tile, and (chunk = 1) the column tiles streamed one at a
+    time through a workspace-sized chunk: equal to the dense kernel and the oracle."""
+    if chunk:
+        monkeypatch.setenv("DOT_SEG_CHUNK", chunk)
+    cfg = small_config(n=(24, 20, 10), L=(4.0, 3.5, 2.5), src=(13, 1), det=(10, 7), n_rbf=4, eps=0.5)
+    prob, wl = small_problem(cfg)
+    g = gpu_problem(dot, cfg, prob, wl)
+    g.reset_stats()
+    Js = g.jacobian(None, None)                     # ld = 70, ls = 13
+    st = g.stats()
+    assert st["contract_flops"] < st["contract_flops_dense"]
+    monkeypatch.setenv("DOT_CONTRACT", "dense")
+    gd = gpu_problem(dot, cfg, prob, wl)
+    Jd = gd.jacobian(None, None)
+    assert rel(Js, Jd) < 1e-12
+    Jo = jacobian(prob, wl.p, np.eye(cfg.n_s), np.eye(cfg.n_d))
+    assert rel(Js, Jo) < 1e-7
