@@ -60,7 +60,7 @@ struct dot_problem {
     DBuf<int32_t> d_seg, d_segoff;    // block sparsity of G by basis (GSparse)
     DBuf<int32_t> d_segslot;          // [T] sample slot of the basis-ordered support points
     DBuf<double> d_Gseg;              // [T][5] basis-ordered weights
-    DBuf<int32_t> d_ktile, d_kto;     // k-tiles of the segment GEMM (GSparse::ktile, ::kto)
+    DBuf<int32_t> d_ktile, d_kto, d_jorder;   // segment GEMM k-tiles / work order (GSparse)
     GSparse gsp;
     DBuf<double2> d_Dt;               // data, [n_freq][n_src][n_det]
     FieldCache cache[2];              // 0: sources, 1: detectors
@@ -1166,8 +1166,8 @@ size_t dot_workspace_bytes(const dot_problem* P, int32_t max_rhs) {
     // the Jacobian's support panels / combined fields, and the host-staged full Jacobian
     fixed += 2 * (size_t)P->n_freq * (P->n_src + P->n_det) * Kb * sizeof(double2);
     fixed += (size_t)P->n_freq * P->n_src * P->n_det * std::max(P->n_p, 1) * sizeof(double2);
-    // one frequency's operand tiles of the segment GEMM (every support point in every basis)
-    fixed += contract_seg_tma_bytes(P->n_det, P->n_src, (long long)Kb * 2, P->n_rbf);
+    // two frequencies' operand tiles of the segment GEMM (support budget Kb points over all bases)
+    fixed += 2 * contract_seg_tma_bytes(P->n_det, P->n_src, (long long)Kb, P->n_rbf);   // double-buffered
     // max_rhs systems = max_rhs / n_freq real seeds (all shifts of one seed together), in pairs
     const size_t pairs = ((size_t)std::max(max_rhs, 1) + 2 * P->n_freq - 1) / (2 * P->n_freq) + 1;
     // dense solutions (dot_solve: every node sampled) of up to 3 complex right-hand sides
@@ -1281,6 +1281,7 @@ int dot_set_params(dot_problem* P, const double* p, int where) {
     P->d_Gseg.reset();
     P->d_ktile.reset();
     P->d_kto.reset();
+    P->d_jorder.reset();
     P->gsp = GSparse{};
     launch_compact(P->d_flagS.get(), P->d_posS.get(), N, P->d_S.get(), s);
     launch_compact(P->d_flagP.get(), P->d_posP.get(), N, P->d_P.get(), s);
@@ -1314,13 +1315,21 @@ int dot_set_params(dot_problem* P, const double* p, int where) {
                 for (int t = hoff[j]; t < hoff[j + 1]; t += 16) {
                     ktile.push_back(t);
                     ktile.push_back(hoff[j + 1]);
+                    ktile.push_back(j);
+                    ktile.push_back(0);
                 }
             }
-            if (ktile.empty()) ktile.assign(2, 0);
+            if (ktile.empty()) ktile.assign(4, 0);
+            std::vector<int32_t> jorder(P->n_rbf);
+            for (int j = 0; j < P->n_rbf; ++j) jorder[j] = j;
+            std::stable_sort(jorder.begin(), jorder.end(),
+                             [&](int a, int b) { return kto[a + 1] - kto[a] > kto[b + 1] - kto[b]; });
             P->d_kto = to_device(P, kto.data(), kto.size(), DOT_HOST);
             P->d_ktile = to_device(P, ktile.data(), ktile.size(), DOT_HOST);
+            P->d_jorder = to_device(P, jorder.data(), std::max<size_t>(jorder.size(), 1), DOT_HOST);
             P->gsp = GSparse{P->d_seg.get(), P->d_segoff.get(), P->n_rbf, T,
-                             reinterpret_cast<const int2*>(P->d_ktile.get()), P->d_kto.get(), kto[P->n_rbf]};
+                             reinterpret_cast<const int4*>(P->d_ktile.get()), P->d_kto.get(), kto[P->n_rbf],
+                             P->d_jorder.get()};
             P->d_segslot = DBuf<int32_t>(P->arena, std::max(T, 1));
             P->d_Gseg = DBuf<double>(P->arena, 5 * (size_t)std::max(T, 1));
             launch_compose_index(P->d_seg.get(), T, P->d_S_slot.get(), P->d_segslot.get(), s);
@@ -1433,7 +1442,7 @@ int dot_jacobian(dot_problem* P, const double* W, int32_t ls, const double* V, i
         contract_seg(P, nf, Kp, ld, ls, LS.get(), (size_t)ld * Kp, US.get(), (size_t)ls * Kp, J);
     else
         launch_contract(nf, K, ld, ls, P->n_p, LS.get(), (size_t)ld * K, US.get(), (size_t)ls * K, P->d_G.get(), J, s,
-                        &P->gsp);
+                        &P->gsp, &P->arena, &P->stats.kernel_launches);
     P->stats.kernel_launches += 3;
     if (P->timing) {
         DOT_CUDA_TRY(cudaEventRecord(e1, s));
@@ -1824,8 +1833,7 @@ int dot_contract_fields(dot_problem* P, int32_t ld, int32_t ls, const double* La
         start_timer();
         launch_contract(nf, K, ld, ls, P->n_p, reinterpret_cast<const double2*>(Lam), (size_t)ld * K,
                         reinterpret_cast<const double2*>(U), (size_t)ls * K, P->d_G.get(), reinterpret_cast<double2*>(J),
-                        s, &P->gsp);
-        P->stats.kernel_launches++;
+                        s, &P->gsp, &P->arena, &P->stats.kernel_launches);
     }
     if (P->timing) {
         DOT_CUDA_TRY(cudaEventRecord(e1, s));

@@ -11,6 +11,9 @@
 // double-buffered in shared memory: the global loads of k-tile t+1 are issued
 // into registers before the DMMAs of tile t and land in the other buffer after
 // them -- one barrier per k-tile.  8 warps, warp w owns rows 16w .. 16w+15.
+#include <map>
+#include <mutex>
+
 #include "arena.h"
 #include "kernels.h"
 
@@ -443,28 +446,41 @@ constexpr size_t SMEM = 128 + (size_t)NST * 2 * BLK;
 static_assert(SMEM <= 232448, "seg_tma_gemm shared memory");
 }  // namespace tma
 
-template <int SIDE>
-__global__ void __launch_bounds__(256) seg_prescale_kernel(int rows, int ls, int T, const double2* __restrict__ P,
+// Blocks [0, nA) of grid.y: A side (detector rows of Lam), blocks [nA, ..): B side rows
+// (q, i) = q ls + i of column tiles rtB0 + (y - nA), weights folded in.
+__global__ void __launch_bounds__(256) seg_prescale_kernel(int ld, int ls, int T, const double2* __restrict__ Lam,
+                                                           const double2* __restrict__ U,
                                                            const double* __restrict__ Gs,
-                                                           const int2* __restrict__ ktile, int KTn, int rt0,
-                                                           unsigned char* out) {
-    const int g = blockIdx.x, rt = rt0 + blockIdx.y;
-    unsigned char* base = out + ((size_t)blockIdx.y * KTn + g) * tma::BLK;
+                                                           const int4* __restrict__ ktile, int KTn, int nA, int rtB0,
+                                                           unsigned char* outA, unsigned char* outB) {
+    const int g = blockIdx.x;
+    const bool bside = (int)blockIdx.y >= nA;
+    const int rt = bside ? rtB0 + (int)blockIdx.y - nA : (int)blockIdx.y;
+    unsigned char* base = bside ? outB + ((size_t)(blockIdx.y - nA) * KTn + g) * tma::BLK
+                                : outA + ((size_t)blockIdx.y * KTn + g) * tma::BLK;
     double2* o2 = reinterpret_cast<double2*>(base);
     double* o1 = reinterpret_cast<double*>(base + tma::QM * tma::KT * 16);
-    const int2 kt = ktile[g];
+    __shared__ int rowq[tma::QM], rowi[tma::QM];
+    if (threadIdx.x < tma::QM) {                 // row -> (q, i) once per block (no per-element divide)
+        const int n = rt * tma::QM + threadIdx.x;
+        const int q = bside ? n / ls : 0;
+        rowq[threadIdx.x] = q;
+        rowi[threadIdx.x] = bside ? n - q * ls : n;
+    }
+    __syncthreads();
+    const int4 kt = ktile[g];
+    const int rows = bside ? 5 * ls : ld;
     for (int e = threadIdx.x; e < tma::QM * tma::KT; e += blockDim.x) {
         const int r = e >> 4, kk = e & 15, n = rt * tma::QM + r, t = kt.x + kk;
         double2 v = make_double2(0.0, 0.0);
         double sm = 0.0;
         if (n < rows && t < kt.y) {
-            if (SIDE == 0) {
-                v = P[(size_t)n * T + t];
+            if (!bside) {
+                v = Lam[(size_t)n * T + t];
                 sm = v.x + v.y;
             } else {
-                const int q = n / ls, i = n - q * ls;
-                const double2 u = P[(size_t)i * T + t];
-                const double w = Gs[(size_t)t * 5 + q];
+                const double2 u = U[(size_t)rowi[r] * T + t];
+                const double w = Gs[(size_t)t * 5 + rowq[r]];
                 v = make_double2(w * u.x, w * u.y);
                 sm = w * (u.x + u.y);
             }
@@ -474,21 +490,28 @@ __global__ void __launch_bounds__(256) seg_prescale_kernel(int rows, int ls, int
     }
 }
 
+// Persistent, dynamically scheduled: the producer lane claims work items from a global
+// counter (items ordered basis jorder[.] largest first, then column tile, then detector tile:
+// longest-first list scheduling) and streams their k-tiles back to back through the ring,
+// tagging each stage with (item, k-tile, k-tiles of the item); the next item's first tiles
+// land during the current item's last DMMAs and epilogue.  An item of a basis without points
+// is a stage with no data (its J block is written as zeros); item -1 ends the CTA.
 __global__ void __launch_bounds__(tma::NT, 1) seg_tma_gemm_kernel(int ld, int ls, int n_p, const unsigned char* Ap,
                                                                  const unsigned char* Bp, int KTn,
-                                                                 const int32_t* __restrict__ kto, int nt0,
-                                                                 double2* J) {
-    using tma::KT;
-    using tma::NST;
-    using tma::NCW;
+                                                                 const int32_t* __restrict__ kto,
+                                                                 const int32_t* __restrict__ jorder, int nDT, int nn,
+                                                                 int nitems, int nt0, int* counter, double2* J) {
     using tma::BLK;
+    using tma::KT;
+    using tma::NCW;
+    using tma::NST;
     constexpr int TM = tma::QM;
     extern __shared__ __align__(128) unsigned char tsm[];
     const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(tsm));   // full[NST], empty[NST]
+    int* meta = reinterpret_cast<int*>(tsm + 16 * NST);                             // [NST][4]
     const uint32_t st0 = bar0 + 128;
-    const int dt = blockIdx.x, ntl = blockIdx.y, j = blockIdx.z;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int g0 = kto[j], nkt = kto[j + 1] - g0;
+    const int per_j = nDT * nn;
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar0 + 8 * s), "r"(1));
@@ -497,25 +520,48 @@ __global__ void __launch_bounds__(tma::NT, 1) seg_tma_gemm_kernel(int ld, int ls
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (warp == NCW) {                                   // producer: one lane streams the blocks
+    if (warp == NCW) {                                   // producer: one lane claims items, streams blocks
         if (lane == 0) {
-            const unsigned char* a = Ap + ((size_t)dt * KTn + g0) * BLK;
-            const unsigned char* b = Bp + ((size_t)ntl * KTn + g0) * BLK;
-            for (int t = 0; t < nkt; ++t) {
-                const int s = t % NST;
-                if (t >= NST) mbar_wait(bar0 + 8 * (NST + s), ((t / NST) - 1) & 1);
+            uint32_t gt = 0;
+            // stage tag: (t, k-tiles of the item, basis j, tile = dt + nDT ntl); j = -1 ends the CTA
+            auto stage = [&](int t, int nkt, int j, int tile, const unsigned char* a, const unsigned char* b) {
+                const uint32_t s = gt % NST;
+                if (gt >= NST) mbar_wait(bar0 + 8 * (NST + s), ((gt / NST) - 1) & 1);
+                meta[4 * s] = t;
+                meta[4 * s + 1] = nkt;
+                meta[4 * s + 2] = j;
+                meta[4 * s + 3] = tile;
                 const uint32_t fb = bar0 + 8 * s, dA = st0 + s * 2 * BLK;
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(2 * BLK)
-                             : "memory");
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dA),
-                    "l"(a + (size_t)t * BLK), "r"(BLK), "r"(fb)
-                    : "memory");
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        dA + BLK),
-                    "l"(b + (size_t)t * BLK), "r"(BLK), "r"(fb)
-                    : "memory");
+                if (a) {
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(2 * BLK)
+                                 : "memory");
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            dA),
+                        "l"(a), "r"(BLK), "r"(fb)
+                        : "memory");
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            dA + BLK),
+                        "l"(b), "r"(BLK), "r"(fb)
+                        : "memory");
+                } else {
+                    mbar_arrive(fb);
+                }
+                ++gt;
+            };
+            for (;;) {
+                const int it = atomicAdd(counter, 1);
+                if (it >= nitems) {
+                    stage(0, 0, -1, 0, nullptr, nullptr);
+                    break;
+                }
+                const int j = jorder[it / per_j], r = it % per_j, ntl = r / nDT, dt = r % nDT;
+                const int g0 = kto[j], nkt = kto[j + 1] - g0;
+                const unsigned char* a = Ap + ((size_t)dt * KTn + g0) * BLK;
+                const unsigned char* b = Bp + ((size_t)ntl * KTn + g0) * BLK;
+                if (nkt == 0) stage(0, 0, j, r, nullptr, nullptr);
+                for (int t = 0; t < nkt; ++t) stage(t, nkt, j, r, a + (size_t)t * BLK, b + (size_t)t * BLK);
             }
         }
         return;
@@ -523,62 +569,141 @@ __global__ void __launch_bounds__(tma::NT, 1) seg_tma_gemm_kernel(int ld, int ls
     const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;
     const int r4 = lane >> 2, sw2 = (r4 & 1) << 2, sw1 = (r4 & 3) << 2;
     double p1[2][4][2], p2[2][4][2], p3[2][4][2];
+    for (uint32_t gt = 0;; ++gt) {
+        const uint32_t s = gt % NST;
+        mbar_wait(bar0 + 8 * s, (gt / NST) & 1);
+        const int t = meta[4 * s], nkt = meta[4 * s + 1], j = meta[4 * s + 2], tile = meta[4 * s + 3];
+        if (j < 0) break;
+        if (t == 0) {
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
+            for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
+                for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) p1[mi][ni][h] = p2[mi][ni][h] = p3[mi][ni][h] = 0.0;
-    for (int t = 0; t < nkt; ++t) {
-        const int s = t % NST;
-        mbar_wait(bar0 + 8 * s, (t / NST) & 1);
-        const unsigned char* sa = tsm + 128 + (size_t)s * 2 * BLK;
-        const double2* A2 = reinterpret_cast<const double2*>(sa);
-        const double* A1 = reinterpret_cast<const double*>(sa + TM * KT * 16);
-        const double2* B2 = reinterpret_cast<const double2*>(sa + BLK);
-        const double* B1 = reinterpret_cast<const double*>(sa + BLK + TM * KT * 16);
+                    for (int h = 0; h < 2; ++h) p1[mi][ni][h] = p2[mi][ni][h] = p3[mi][ni][h] = 0.0;
+        }
+        if (nkt > 0) {
+            const unsigned char* sa = tsm + 128 + (size_t)s * 2 * BLK;
+            const double2* A2 = reinterpret_cast<const double2*>(sa);
+            const double* A1 = reinterpret_cast<const double*>(sa + TM * KT * 16);
+            const double2* B2 = reinterpret_cast<const double2*>(sa + BLK);
+            const double* B1 = reinterpret_cast<const double*>(sa + BLK + TM * KT * 16);
 #pragma unroll
-        for (int k4 = 0; k4 < KT; k4 += 4) {
-            const int kk = k4 + (lane & 3);
-            double2 a[2];
-            double as[2];
-#pragma unroll
-            for (int mi = 0; mi < 2; ++mi) {
-                const int r = wm + mi * 8 + r4;
-                a[mi] = A2[r * 16 + (kk ^ sw2)];
-                as[mi] = A1[r * 16 + (kk ^ sw1)];
-            }
-#pragma unroll
-            for (int ni = 0; ni < 4; ++ni) {
-                const int r = wn + ni * 8 + r4;
-                const double2 b = B2[r * 16 + (kk ^ sw2)];
-                const double bs = B1[r * 16 + (kk ^ sw1)];
+            for (int k4 = 0; k4 < KT; k4 += 4) {
+                const int kk = k4 + (lane & 3);
+                double2 a[2];
+                double as[2];
 #pragma unroll
                 for (int mi = 0; mi < 2; ++mi) {
-                    dmma(p1[mi][ni][0], p1[mi][ni][1], a[mi].x, b.x);
-                    dmma(p2[mi][ni][0], p2[mi][ni][1], a[mi].y, b.y);
-                    dmma(p3[mi][ni][0], p3[mi][ni][1], as[mi], bs);
+                    const int rr = wm + mi * 8 + r4;
+                    a[mi] = A2[rr * 16 + (kk ^ sw2)];
+                    as[mi] = A1[rr * 16 + (kk ^ sw1)];
+                }
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) {
+                    const int rr = wn + ni * 8 + r4;
+                    const double2 b = B2[rr * 16 + (kk ^ sw2)];
+                    const double bs = B1[rr * 16 + (kk ^ sw1)];
+#pragma unroll
+                    for (int mi = 0; mi < 2; ++mi) {
+                        dmma(p1[mi][ni][0], p1[mi][ni][1], a[mi].x, b.x);
+                        dmma(p2[mi][ni][0], p2[mi][ni][1], a[mi].y, b.y);
+                        dmma(p3[mi][ni][0], p3[mi][ni][1], as[mi], bs);
+                    }
                 }
             }
         }
         mbar_arrive(bar0 + 8 * (NST + s));
+        if (t + 1 < nkt) continue;
+        // last k-tile of the item: epilogue J[(d, i)][5 j + q] = -C[d][q ls + i]
+        const int ntl = tile / nDT, dt = tile - ntl * nDT;
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+            const int d = dt * TM + wm + mi * 8 + r4;
+            if (d >= ld) continue;
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int n = (nt0 + ntl) * TM + wn + ni * 8 + 2 * (lane & 3) + h;
+                    if (n >= 5 * ls) continue;
+                    const int q = n / ls, i = n - q * ls;
+                    const double re = p1[mi][ni][h] - p2[mi][ni][h];
+                    const double im = p3[mi][ni][h] - p1[mi][ni][h] - p2[mi][ni][h];
+                    J[((size_t)d * ls + i) * n_p + 5 * j + q] = make_double2(-re, -im);
+                }
+        }
     }
-    // epilogue: J[(d, i)][5 j + q] = -C[d][q ls + i]
+}
+
+// ---------------------------------------------- small panels: split over the k-tiles
+// The sketched and optimized-direction contractions have ld x ls <= 256 pairs (12 x 12 at
+// the BASELINE configs): a GEMM tile would be mostly padding and 16 bases x n_freq tiles
+// cannot fill 148 SMs.  One CTA per (k-tile of 16 points of one basis, frequency) forms
+// the partial sums of all ld x ls x 5 outputs of that basis over its 16 points (FP64 FMA on
+// shared-memory copies of the fields at those points); a second kernel adds the partials of
+// each basis in k-tile order (deterministic, no atomics) into J.
+constexpr int SMALL_PAIRS = 256, SMALL_ROWS = 160;   // ld * ls and ld + ls limits of the small form
+
+__global__ void __launch_bounds__(256) contract_small_kernel(int K, int ld, int ls, int n_p,
+                                                             const double2* __restrict__ Lam, size_t lam_bs,
+                                                             const double2* __restrict__ U, size_t u_bs,
+                                                             const double* __restrict__ G,
+                                                             const int32_t* __restrict__ seg,
+                                                             const int4* __restrict__ ktile, int KTn,
+                                                             double2* __restrict__ part) {
+    __shared__ double2 sf[SMALL_ROWS][16];                 // rows [0, ld): Lam, [ld, ld + ls): U
+    __shared__ double sg[16][5];
+    const int g = blockIdx.x, f = blockIdx.y;
+    const int4 kt = ktile[g];
+    const int np = min(16, kt.y - kt.x);
+    const double2* Lf = Lam + (size_t)f * lam_bs;
+    const double2* Uf = U + (size_t)f * u_bs;
+    for (int e = threadIdx.x; e < (ld + ls) * 16; e += blockDim.x) {
+        const int r = e >> 4, t = e & 15;
+        double2 v = make_double2(0.0, 0.0);
+        if (t < np) {
+            const int node = seg[kt.x + t];
+            v = r < ld ? Lf[(size_t)r * K + node] : Uf[(size_t)(r - ld) * K + node];
+        }
+        sf[r][t] = v;
+    }
+    if (threadIdx.x < 80) {
+        const int t = threadIdx.x / 5, q = threadIdx.x % 5;
+        sg[t][q] = t < np ? G[(size_t)seg[kt.x + t] * n_p + 5 * kt.z + q] : 0.0;
+    }
+    __syncthreads();
+    const int nout = ld * ls * 5;
+    double2* out = part + ((size_t)f * KTn + g) * nout;
+    for (int o = threadIdx.x; o < nout; o += blockDim.x) {
+        const int q = o % 5, pr = o / 5, d = pr / ls, i = pr - d * ls;
+        double re = 0.0, im = 0.0;
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi) {
-        const int d = dt * TM + wm + mi * 8 + r4;
-        if (d >= ld) continue;
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int n = (nt0 + ntl) * TM + wn + ni * 8 + 2 * (lane & 3) + h;
-                if (n >= 5 * ls) continue;
-                const int q = n / ls, i = n - q * ls;
-                const double re = p1[mi][ni][h] - p2[mi][ni][h];
-                const double im = p3[mi][ni][h] - p1[mi][ni][h] - p2[mi][ni][h];
-                J[((size_t)d * ls + i) * n_p + 5 * j + q] = make_double2(-re, -im);
-            }
+        for (int t = 0; t < 16; ++t) {
+            const double2 h = cmul(sf[d][t], sf[ld + i][t]);
+            re = fma(h.x, sg[t][q], re);
+            im = fma(h.y, sg[t][q], im);
+        }
+        out[o] = make_double2(re, im);
+    }
+}
+
+__global__ void contract_small_reduce_kernel(int nb, int ld, int ls, int n_p, const double2* __restrict__ part,
+                                             const int32_t* __restrict__ kto, int KTn, double2* J) {
+    const size_t tot = (size_t)nb * ld * ls * n_p;
+    const int nout = ld * ls * 5;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
+        const int k = (int)(e % n_p);
+        const size_t fp = e / n_p;                       // f * npairs + pair
+        const int f = (int)(fp / ((size_t)ld * ls)), pr = (int)(fp % ((size_t)ld * ls));
+        const int j = k / 5, o = pr * 5 + k % 5;
+        double re = 0.0, im = 0.0;
+        for (int g = kto[j]; g < kto[j + 1]; ++g) {
+            const double2 v = part[((size_t)f * KTn + g) * nout + o];
+            re += v.x;
+            im += v.y;
+        }
+        J[e] = make_double2(-re, -im);
     }
 }
 
@@ -669,6 +794,21 @@ size_t contract_seg_tma_bytes(int ld, int ls, long long total, int n_rbf) {
     return ((size_t)(ld + tma::QM - 1) / tma::QM + (5 * (size_t)ls + tma::QM - 1) / tma::QM) * kts * tma::BLK;
 }
 
+// Side stream of the current device for the operand prescale (created once, non-blocking).
+static cudaStream_t prescale_stream() {
+    static std::mutex mtx;
+    static std::map<int, cudaStream_t> streams;
+    int dev = 0;
+    DOT_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mtx);
+    auto it = streams.find(dev);
+    if (it != streams.end()) return it->second;
+    cudaStream_t st = nullptr;
+    DOT_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    streams[dev] = st;
+    return st;
+}
+
 void contract_seg_tma(int nb, int T, int ld, int ls, int n_p, const double2* Lam, size_t lam_bstride,
                       const double2* U, size_t u_bstride, const double* Gs, const GSparse& sp, double2* J,
                       Arena& arena, cudaStream_t s, int64_t* launches) {
@@ -681,26 +821,65 @@ void contract_seg_tma(int nb, int T, int ld, int ls, int n_p, const double2* Lam
     const int KTn = sp.ktiles;
     const int nDT = (ld + tma::QM - 1) / tma::QM, nNT = (5 * ls + tma::QM - 1) / tma::QM;
     const size_t per_tile = (size_t)KTn * tma::BLK;
+    const size_t set_bytes = (size_t)(nDT + nNT) * per_tile;       // one frequency's A and B tiles
+    ensure_smem(seg_tma_gemm_kernel, tma::SMEM);
+    int sms = 0, dev = 0;
+    DOT_CUDA_TRY(cudaGetDevice(&dev));
+    DOT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    auto gemm = [&](int f, const unsigned char* A, const unsigned char* B, int nt0, int nn, int* counter) {
+        const int nitems = sp.n_rbf * nDT * nn;
+        seg_tma_gemm_kernel<<<std::min(nitems, sms), tma::NT, tma::SMEM, s>>>(
+            ld, ls, n_p, A, B, KTn, sp.kto, sp.jorder, nDT, nn, nitems, nt0, counter, J + (size_t)f * npairs * n_p);
+        DOT_CUDA_TRY(cudaGetLastError());
+    };
+    auto prescale = [&](int f, unsigned char* A, unsigned char* B, int nA, int nt0, int nn, cudaStream_t st) {
+        seg_prescale_kernel<<<dim3(KTn, nA + nn), 256, 0, st>>>(ld, ls, T, Lam + (size_t)f * lam_bstride,
+                                                               U + (size_t)f * u_bstride, Gs, sp.ktile, KTn, nA, nt0,
+                                                               A, B);
+        DOT_CUDA_TRY(cudaGetLastError());
+    };
+    const bool chunk_env = std::getenv("DOT_SEG_CHUNK") != nullptr;       // tests: force the chunked path
+    if (nb > 1 && !chunk_env && arena.largest_free() >= 2 * set_bytes + (64u << 20)) {
+        // two operand sets: the prescale of frequency f+1 (memory-bound, side stream) runs while
+        // the GEMM of frequency f (DMMA-bound) owns the SMs' tensor pipes
+        DBuf<unsigned char> buf[2] = {DBuf<unsigned char>(arena, set_bytes), DBuf<unsigned char>(arena, set_bytes)};
+        DBuf<int> counters(arena, nb);
+        DOT_CUDA_TRY(cudaMemsetAsync(counters.get(), 0, nb * sizeof(int), s));
+        cudaStream_t s2 = prescale_stream();
+        cudaEvent_t ev[5];
+        for (auto& e : ev) DOT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        cudaEvent_t &in_ready = ev[0], *pre = ev + 1, *used = ev + 3;
+        DOT_CUDA_TRY(cudaEventRecord(in_ready, s));
+        DOT_CUDA_TRY(cudaStreamWaitEvent(s2, in_ready, 0));
+        for (int f = 0; f < nb; ++f) {
+            const int b = f & 1;
+            unsigned char* A = buf[b].get();
+            unsigned char* B = A + (size_t)nDT * per_tile;
+            if (f >= 2) DOT_CUDA_TRY(cudaStreamWaitEvent(s2, used[b], 0));     // GEMM f-2 done with buf b
+            prescale(f, A, B, nDT, 0, nNT, s2);
+            DOT_CUDA_TRY(cudaEventRecord(pre[b], s2));
+            DOT_CUDA_TRY(cudaStreamWaitEvent(s, pre[b], 0));
+            gemm(f, A, B, 0, nNT, counters.get() + f);
+            DOT_CUDA_TRY(cudaEventRecord(used[b], s));
+            *launches += 2;
+        }
+        for (auto& e : ev) DOT_CUDA_TRY(cudaEventDestroy(e));   // released once their work completes
+        return;
+    }
+    // one operand set; B tiles of a frequency in chunks of column tiles when the workspace is short
     DBuf<unsigned char> Ap(arena, nDT * per_tile);
-    // B operand tiles: all column tiles of a frequency if the workspace holds them, else chunks
     const size_t room = arena.largest_free();
     int chunk = (int)std::max<size_t>(1, std::min<size_t>(nNT, room > per_tile ? room / per_tile : 1));
-    if (const char* e = std::getenv("DOT_SEG_CHUNK")) chunk = std::max(1, std::min(chunk, std::atoi(e)));  // tests
+    if (chunk_env) chunk = std::max(1, std::min(chunk, std::atoi(std::getenv("DOT_SEG_CHUNK"))));
     DBuf<unsigned char> Bp(arena, (size_t)chunk * per_tile);
-    ensure_smem(seg_tma_gemm_kernel, tma::SMEM);
+    const int nch = (nNT + chunk - 1) / chunk;
+    DBuf<int> counters(arena, (size_t)nb * nch);
+    DOT_CUDA_TRY(cudaMemsetAsync(counters.get(), 0, (size_t)nb * nch * sizeof(int), s));
     for (int f = 0; f < nb; ++f) {
-        seg_prescale_kernel<0><<<dim3(KTn, nDT), 256, 0, s>>>(ld, ls, T, Lam + (size_t)f * lam_bstride, Gs, sp.ktile, KTn,
-                                                             0, Ap.get());
-        DOT_CUDA_TRY(cudaGetLastError());
-        *launches += 1;
         for (int nt0 = 0; nt0 < nNT; nt0 += chunk) {
             const int nn = std::min(chunk, nNT - nt0);
-            seg_prescale_kernel<1><<<dim3(KTn, nn), 256, 0, s>>>(5 * ls, ls, T, U + (size_t)f * u_bstride, Gs,
-                                                                sp.ktile, KTn, nt0, Bp.get());
-            DOT_CUDA_TRY(cudaGetLastError());
-            seg_tma_gemm_kernel<<<dim3(nDT, nn, sp.n_rbf), tma::NT, tma::SMEM, s>>>(
-                ld, ls, n_p, Ap.get(), Bp.get(), KTn, sp.kto, nt0, J + (size_t)f * npairs * n_p);
-            DOT_CUDA_TRY(cudaGetLastError());
+            prescale(f, Ap.get(), Bp.get(), nt0 == 0 ? nDT : 0, nt0, nn, s);   // A tiles once per frequency
+            gemm(f, Ap.get(), Bp.get(), nt0, nn, counters.get() + f * nch + nt0 / chunk);
             *launches += 2;
         }
     }
@@ -708,13 +887,31 @@ void contract_seg_tma(int nb, int T, int ld, int ls, int n_p, const double2* Lam
 
 void launch_contract(int nb, int K, int ld, int ls, int n_p, const double2* Lam, size_t lam_bstride,
                      const double2* U, size_t u_bstride, const double* G, double2* J, cudaStream_t s,
-                     const GSparse* sp) {
+                     const GSparse* sp, Arena* arena, int64_t* launches) {
     const int npairs = ld * ls;
     if (nb <= 0 || npairs <= 0 || n_p <= 0) return;
     if (K <= 0) {
         DOT_CUDA_TRY(cudaMemsetAsync(J, 0, (size_t)nb * npairs * n_p * sizeof(double2), s));
         return;
     }
+    if (sp && sp->seg && sp->ktile && sp->n_rbf * 5 == n_p && arena && npairs <= SMALL_PAIRS && ld + ls <= SMALL_ROWS) {
+        const int KTn = sp->ktiles;
+        if (KTn == 0) {
+            DOT_CUDA_TRY(cudaMemsetAsync(J, 0, (size_t)nb * npairs * n_p * sizeof(double2), s));
+            return;
+        }
+        DBuf<double2> part(*arena, (size_t)nb * KTn * npairs * 5);
+        contract_small_kernel<<<dim3(KTn, nb), 256, 0, s>>>(K, ld, ls, n_p, Lam, lam_bstride, U, u_bstride, G, sp->seg,
+                                                           sp->ktile, KTn, part.get());
+        DOT_CUDA_TRY(cudaGetLastError());
+        const size_t tot = (size_t)nb * npairs * n_p;
+        contract_small_reduce_kernel<<<(unsigned)std::min<size_t>((tot + 255) / 256, 4096), 256, 0, s>>>(
+            nb, ld, ls, n_p, part.get(), sp->kto, KTn, J);
+        DOT_CUDA_TRY(cudaGetLastError());
+        if (launches) *launches += 2;
+        return;
+    }
+    if (launches) *launches += 1;
     if (sp && sp->seg && sp->n_rbf * 5 == n_p) {
         dim3 grid((npairs + BM / 2 - 1) / (BM / 2), sp->n_rbf, nb);
         const size_t smem = (size_t)(2 * BM * SAS + 2 * SBK * SGS) * sizeof(double);

@@ -123,17 +123,23 @@ struct GSparse {
     const int32_t* segoff = nullptr;   // [n_rbf + 1]
     int n_rbf = 0;
     long long total = 0;               // segoff[n_rbf]
-    // k-tiles of 16 basis-ordered points that never straddle two bases (contract_seg_tma):
-    // ktile[g] = (first point, end of its basis's points), kto[j] = first k-tile of basis j
-    const int2* ktile = nullptr;
+    // k-tiles of 16 basis-ordered points that never straddle two bases (contract_seg_tma,
+    // contract_small): ktile[g] = (first point, end of its basis's points, basis j, 0),
+    // kto[j] = first k-tile of basis j
+    const int4* ktile = nullptr;
     const int32_t* kto = nullptr;      // [n_rbf + 1]
     int ktiles = 0;                    // kto[n_rbf]
+    const int32_t* jorder = nullptr;   // [n_rbf] bases by decreasing k-tile count (work order)
 };
 // sp == null (or no segments): dense DMMA contraction over all K points; else the
 // block-sparse one (per basis j, its support points only).
+// With `arena` and small panels (ld * ls <= 256: the sketched / optimized-direction shapes) the
+// block-sparse form runs split over the k-tiles (contract_small_kernel) with a fixed-order
+// reduction; launches are added to *launches when given.
 void launch_contract(int nb, int K, int ld, int ls, int n_p, const double2* Lam, size_t lam_bstride,
                      const double2* U, size_t u_bstride, const double* G, double2* J,
-                     cudaStream_t s, const GSparse* sp = nullptr);
+                     cudaStream_t s, const GSparse* sp = nullptr, Arena* arena = nullptr,
+                     int64_t* launches = nullptr);
 // Block-sparse GEMM on basis-ordered panels (the default for large panels): Lam [nb][ld][T],
 // U [nb][ls][T] with column t the support point seg[t] of basis j (segoff[j] <= t < segoff[j+1]),
 // Gs [T][5] the basis's weights there.  contract_seg_applies: the panel shape takes this path.

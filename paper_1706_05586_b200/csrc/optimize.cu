@@ -216,8 +216,9 @@ double optimize_two_phase(OptContext& c, int k, std::vector<double>& W, int ls, 
             launch_rc_gemm(nf, b, K, nd, dV.get(), b, LS.get(), (size_t)nd * K, K, 1, LV.get(), (size_t)b * K, K, 1, s);
             lam = LV.get();
         }
-        launch_contract(nf, K, b, a, n_p, lam, (size_t)b * K, u, (size_t)a * K, c.G, J.get(), s, c.gsp);
-        *c.launches += 3;
+        launch_contract(nf, K, b, a, n_p, lam, (size_t)b * K, u, (size_t)a * K, c.G, J.get(), s, c.gsp, &c.arena,
+                        c.launches);
+        *c.launches += 2;
         DOT_CUDA_TRY(cudaStreamSynchronize(s));   // host copies above must outlive their async use
         return J;
     };
@@ -357,8 +358,8 @@ double optimize_two_phase_subspace(OptContext& c, SubspaceOps& ops, int k, int i
 
     auto contract = [&](const double2* lam, int nl, const double2* u, int nu) {
         DBuf<double2> J(c.arena, std::max<size_t>((size_t)nf * nl * nu * n_p, 1));
-        launch_contract(nf, K, nl, nu, n_p, lam, (size_t)nl * K, u, (size_t)nu * K, c.G, J.get(), s, c.gsp);
-        *c.launches += 1;
+        launch_contract(nf, K, nl, nu, n_p, lam, (size_t)nl * K, u, (size_t)nu * K, c.G, J.get(), s, c.gsp, &c.arena,
+                        c.launches);
         return J;
     };
     // new fields F' [nf][m][K] = sum_j Gam[j][m] F[f][j][K]  (Gam host [ncols][m])
