@@ -485,8 +485,10 @@ __global__ void __launch_bounds__(256) seg_prescale_kernel(int ld, int ls, int T
                 sm = w * (u.x + u.y);
             }
         }
-        o2[r * 16 + (kk ^ ((r & 1) << 2))] = v;
-        o1[r * 16 + (kk ^ ((r & 3) << 2))] = sm;
+        // streaming stores: the blocks of the next frequency must not evict the operands the
+        // concurrent GEMM of the current frequency re-reads from L2
+        __stcs(o2 + r * 16 + (kk ^ ((r & 1) << 2)), v);
+        __stcs(o1 + r * 16 + (kk ^ ((r & 3) << 2)), sm);
     }
 }
 
