@@ -339,6 +339,7 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, c
         a.samp_off = samp_off;
         a.nP = nP;
         a.H = H.get();
+        set_pass_tmaps(a);
         FoldArgs fa;
         fa.s0 = 0;
         fa.s1 = nP;
@@ -890,6 +891,7 @@ void dd_solve(dot_dd* G, const std::vector<Req>& reqs) {
         a.nzch_tot = pl.C;
         a.zc0 = pl.cb[r];
         a.nzch = pl.cb[r + 1] - pl.cb[r];
+        set_pass_tmaps(a);
         FoldArgs& fa = b.fa;
         fa.s0 = (int)(std::lower_bound(hsamp.begin(), hsamp.end(), (int32_t)((size_t)b.zs * PS)) - hsamp.begin());
         fa.s1 = (int)(std::lower_bound(hsamp.begin(), hsamp.end(), (int32_t)((size_t)b.ze * PS)) - hsamp.begin());
@@ -1120,8 +1122,9 @@ int dot_create(const dot_config* cfg, dot_problem** out) {
             const char* eTY = std::getenv("DOT_CG_TY");
             const char* eRW = std::getenv("DOT_CG_ROWS");
             const char* eNM = std::getenv("DOT_CG_NOMU");
+            const char* eXS = std::getenv("DOT_CG_XS");
             P->tl = cg_tiling(P->nx, P->ny, P->nz, ePD ? std::max(1, std::atoi(ePD)) : 2, eTY ? std::atoi(eTY) : 0,
-                              eRW ? std::atoi(eRW) : 0, eNM && std::atoi(eNM) != 0);
+                              eRW ? std::atoi(eRW) : 0, eNM && std::atoi(eNM) != 0, eXS ? std::atoi(eXS) : 0);
         }
         P->pc = PalsConst{P->nx, P->ny, P->nz, P->n_rbf, P->hx, P->hy, P->hz, P->gamma, P->eps, P->cutoff,
                           P->mua_in, P->mua_out};
@@ -1337,7 +1340,7 @@ int dot_set_params(dot_problem* P, const double* p, int where) {
             P->stats.kernel_launches += 2;
         }
     }
-    launch_sample_offsets(P->d_P.get(), P->nP, P->nx, P->ny, P->nz, P->tl.TY, P->tl.ntiles, P->d_off.get(), s);
+    launch_sample_offsets(P->d_P.get(), P->nP, P->nx, P->ny, P->nz, P->tl.TY, P->tl.nty, P->d_off.get(), s);
     P->stats.kernel_launches += 6;
     sync(P);
     P->have_params = true;
@@ -1643,7 +1646,7 @@ int dot_solve(dot_problem* P, int32_t nrhs, const int32_t* freq, const double* b
     for (size_t i = 0; i < P->N; ++i) all[i] = (int32_t)i;
     DBuf<int32_t> dall = to_device(P, all.data(), all.size(), DOT_HOST);
     DBuf<int32_t> doff(P->arena, (size_t)P->nz * P->tl.ntiles + 1);
-    launch_sample_offsets(dall.get(), (int)P->N, P->nx, P->ny, P->nz, P->tl.TY, P->tl.ntiles, doff.get(), P->stream);
+    launch_sample_offsets(dall.get(), (int)P->N, P->nx, P->ny, P->nz, P->tl.TY, P->tl.nty, doff.get(), P->stream);
     DBuf<double2> dx(P->arena, n);
     auto it = solve_batch(P, {}, db.get(), fh, dx.get(), nrhs, (int)P->N, dall.get(), doff.get());
     from_device(P, reinterpret_cast<double2*>(x), dx.get(), n, where);

@@ -36,8 +36,11 @@
 //   phase 1   plane f:   p_k = r_k + beta p_{k-1}, written in place into the slot
 //   phase 2   plane f-1: q = K~ p_k, r_{k+1} = r_k - alpha q -> Rbuf[(f-1) % 3]; r_k at samples
 //   phase 3   plane f-2: K~ r_{k+1}, reductions, store r_{k+1}
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "kernels.h"
@@ -240,8 +243,9 @@ struct IC {
 
 // Slot layout (per ring slot): r [rowsP*nx] double2 | p [rowsP*nx] double2 | mu [rowsP*nx] double
 // (mu rides along in the same bulk-copy group when MUT; else it is loaded per thread).
-// NX_, TY_: compile-time row length and tile height of the bench geometries (0: run time).
-template <int MAXT, int NS, bool MUT, int RPT, bool ZC, int NX_, int TY_>
+// NX_, TY_, XS_: compile-time slot row length, tile height and x parts of the bench geometries
+// (0: run time).
+template <int MAXT, int NS, bool MUT, int RPT, bool ZC, int NX_, int TY_, int XS_>
 __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant__ PassArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int PD = NS - 2;                          // TMA planes in flight
@@ -249,7 +253,14 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
     const int tile = blockIdx.x % ntiles, zc = a.zc0 + blockIdx.x / ntiles;
     const int pair = a.act ? a.act[blockIdx.y] : blockIdx.y;       // active-list compaction (tail passes)
     if (pair < 0) return;                                          // slot past the active count
-    const int nx = NX_ ? NX_ : a.op.nx, ny = a.op.ny, nz = a.op.nz;
+    // x split (wide rows): tile = (row tile ty, x part xp); the slot rows are nx = the part's
+    // xw columns plus 2 halo columns on each side (local column c = global column cx0 + c)
+    constexpr bool XS1 = XS_ == 1;                     // compile-time: no x split
+    const int xs = XS1 ? 1 : (XS_ ? XS_ : a.tl.xs), ty = XS1 ? tile : tile / xs, xp = XS1 ? 0 : tile - ty * xs;
+    const int nxg = (XS_ == 1 && NX_) ? NX_ : a.op.nx, ny = a.op.ny, nz = a.op.nz;   // global row length
+    const int nx = NX_ ? NX_ : a.tl.nxl;
+    const int xw = XS1 ? nxg : (nxg + xs - 1) / xs, x0 = XS1 ? 0 : xp * xw, x1 = XS1 ? nxg : min(x0 + xw, nxg);
+    const int cx0 = xs > 1 ? x0 - 2 : 0;
     const int TY = TY_ ? TY_ : a.tl.TY;
     // z chunk [z0, z1) of this CTA; phase 1 runs on [a1, b1), phase 2 on [a2, b2)
     // (two / one halo planes recomputed on each side)
@@ -258,10 +269,12 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
     const int a2 = ZC ? max(z0 - 1, 0) : 0, b2 = ZC ? min(z1 + 1, nz) : nz;
     const int fend = ZC ? min(b1, z1) + 2 : nz + 2;
     const int rowsP = TY + 4, rowsR = TY + 2;
-    const int PS = nx * ny;
+    const int PS = nxg * ny;
     const size_t N = (size_t)PS * nz;
-    const int j0 = tile * TY;
-    const int slotE = rowsP * nx;                       // double2 elements of one vector in a slot
+    const int j0 = ty * TY;
+    // double2 elements of one vector in a slot (x split: a multiple of 16, so that every slot and
+    // each vector inside it starts 128-byte aligned for the tensor copies)
+    const int slotE = xs > 1 ? (rowsP * nx + 15) / 16 * 16 : rowsP * nx;
     const int slotW = 2 * slotE + (MUT ? (slotE + 1) / 2 : 0);   // slot stride in double2
     const int rbE = rowsR * nx;
 
@@ -297,7 +310,8 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
         }
         if (a.nP > 0)
             for (int g = threadIdx.x; g < nz; g += blockDim.x)
-                s_samp[g] = make_int2(a.samp_off[g * ntiles + tile], a.samp_off[g * ntiles + tile + 1]);
+                s_samp[g] = XS1 ? make_int2(a.samp_off[g * ntiles + tile], a.samp_off[g * ntiles + tile + 1])
+                                : make_int2(a.samp_off[g * a.tl.nty + ty], a.samp_off[g * a.tl.nty + ty + 1]);
     }
     if (threadIdx.x == 0) {
         for (int q = 0; q < NS; ++q)
@@ -315,10 +329,11 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
 
     // in-domain slot rows [rlo, rhi); grid row of slot row r is j0 - 2 + r
     const int rlo = max(0, 2 - j0), rhi = min(rowsP, ny - j0 + 2);
-    const uint32_t tile_bytes = (uint32_t)((rhi - rlo) * nx * sizeof(double2));
+    const uint32_t tile_bytes = xs > 1 ? (uint32_t)(rowsP * nx * sizeof(double2))     // full box (zero fill)
+                                       : (uint32_t)((rhi - rlo) * nx * sizeof(double2));
     const uint32_t mu_bytes = tile_bytes / 2;
     const uint32_t tx_bytes = 2 * tile_bytes + (MUT ? mu_bytes : 0);
-    const int tile_off = (j0 - 2 + rlo) * nx;
+    const int tile_off = (j0 - 2 + rlo) * nxg;
     const uint32_t slot0 = smem_u32(slots + rlo * nx);             // r rows of slot 0
     const uint32_t slot_stride = (uint32_t)(slotW * sizeof(double2));
     const uint32_t pvec_off = (uint32_t)(slotE * sizeof(double2));
@@ -326,10 +341,33 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
     const uint32_t mu_off = (uint32_t)(2 * slotE * sizeof(double2)) - (uint32_t)(rlo * nx * 8);
     const uint32_t bar0 = smem_u32(bars);
 
-    auto issue = [&](int z, int sl) {      // one thread: bulk copies of contiguous rows
+    // one thread: bulk copies of the contiguous in-domain rows, or (x split) one tensor copy per
+    // vector of the whole (TY + 4) x nxl box
+    auto issue = [&](int z, int sl) {
         const uint32_t dR = slot0 + sl * slot_stride, bar = bar0 + 8 * sl;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx_bytes) : "memory");
+        if (xs > 1) {
+            const uint32_t d0 = smem_u32(slots) + sl * slot_stride;
+            const int cx = cx0, cy = j0 - 2;
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+                "[%6];" ::"r"(d0),
+                "l"(reinterpret_cast<uint64_t>(&a.tmR[kin])), "r"(2 * cx), "r"(cy), "r"(z), "r"(pair), "r"(bar)
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+                "[%6];" ::"r"(d0 + pvec_off),
+                "l"(reinterpret_cast<uint64_t>(&a.tmP[kin])), "r"(2 * cx), "r"(cy), "r"(z), "r"(pair), "r"(bar)
+                : "memory");
+            if (MUT)
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+                    "[%5];" ::"r"(d0 + (uint32_t)(2 * slotE * sizeof(double2))),
+                    "l"(reinterpret_cast<uint64_t>(&a.tmMu)), "r"(cx), "r"(cy), "r"(z), "r"(bar)
+                    : "memory");
+            return;
+        }
         const size_t g = (size_t)z * PS + tile_off;
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dR),
@@ -354,14 +392,17 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
     const int t = threadIdx.x;
     const int m = t / nx, x = t - m * nx;
     const int r0 = RPT * m;
+    const int xg = cx0 + x;                            // global column
+    const bool inx = XS1 || (xg >= 0 && xg < nxg), ownx = XS1 || (xg >= x0 && xg < x1);
+    const bool ph2x = XS1 || (xg >= x0 - 1 && xg <= x1);
     bool indom[RPT], own[RPT], ph2[RPT];
     bool any_in = false, any2 = false, any_own = false;
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
         const int r = r0 + j;
-        indom[j] = r < rowsP && r >= rlo && r < rhi;
-        own[j] = indom[j] && r >= 2 && r < TY + 2;
-        ph2[j] = own[j] || (indom[j] && (r == 1 || r == TY + 2));
+        indom[j] = r < rowsP && r >= rlo && r < rhi && inx;
+        own[j] = indom[j] && r >= 2 && r < TY + 2 && ownx;
+        ph2[j] = XS1 ? (own[j] || (indom[j] && (r == 1 || r == TY + 2))) : (indom[j] && r >= 1 && r <= TY + 2 && ph2x);
         any_in |= indom[j];
         any2 |= ph2[j];
         any_own |= own[j];
@@ -374,8 +415,8 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
     }
     const int o = r0 * nx + x;                         // slot element of row 0
     const int o3 = o - nx;                             // Rbuf element of row 0
-    const int go = (j0 - 2 + r0) * nx + x;             // plane offset of row 0 (may be outside; unused then)
-    const bool hasW = x > 0, hasE = x < nx - 1;
+    const int go = (j0 - 2 + r0) * nxg + xg;           // plane offset of row 0 (may be outside; unused then)
+    const bool hasW = xg > 0, hasE = xg < nxg - 1;
     // running per-thread global pointers (advance one plane per step)
     double2* pP = a.Pv[kout] + (size_t)pair * N + go + (ptrdiff_t)a1 * PS;        // p_k at plane f
     double2* pR = a.R[kout] + (size_t)pair * N + go + (ptrdiff_t)(a1 - 2) * PS;   // r_{k+1} at plane f - 2
@@ -413,7 +454,7 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
         if (!MUT && f < b1)
 #pragma unroll
             for (int j = 0; j < RPT; ++j)
-                if (ph2[j]) MU[j][i0] = pMu[(size_t)f * PS + j * nx];
+                if (ph2[j]) MU[j][i0] = pMu[(size_t)f * PS + j * nxg];
         // ---- phase 1: plane f
         // (zeros are assigned only on the paths that need them: rows outside the domain, and
         // the tail steps past the last plane -- no per-step register clears)
@@ -441,7 +482,7 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
                         const double2 pv = sr[slotE + j * nx];
                         pf[j] = cmk(fma(beta.x, pv.x, rf.x), fma(beta.y, pv.y, rf.y));
                         sr[slotE + j * nx] = pf[j];
-                        if (own[j] && ownf) pP[j * nx] = pf[j];
+                        if (own[j] && ownf) pP[j * nxg] = pf[j];
                     }
                 };
                 if (all_in) p1(IC<1>());
@@ -522,7 +563,12 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
                 const int2 sr2 = s_samp[g];
                 for (int si = sr2.x + threadIdx.x; si < sr2.y; si += blockDim.x) {
                     const int rem = a.samp_nodes[si] - g * PS;
-                    Hk[si] = sr[rem - (j0 - 2) * nx];
+                    if (xs == 1) {
+                        Hk[si] = sr[rem - (j0 - 2) * nx];
+                    } else {
+                        const int row = rem / nxg, col = rem - row * nxg;
+                        if (col >= x0 && col < x1) Hk[si] = sr[(row - (j0 - 2)) * nx + (col - cx0)];
+                    }
                 }
             }
         } else {
@@ -561,7 +607,7 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
                 acc[1] = fma(r0v.y, r0v.y, acc[1]);
                 acc[2] = fma(r0v.x, ar.x, acc[2]);
                 acc[3] = fma(r0v.y, ar.y, acc[3]);
-                pR[j * nx] = r0v;
+                pR[j * nxg] = r0v;
             }
         }
 #pragma unroll
@@ -856,49 +902,75 @@ __global__ void pack_planes_kernel(const double2* A, const double2* B, size_t N,
 
 }  // namespace
 
-size_t pass_smem(int nx, int TY, int NS, int nz, bool mut) {
-    const size_t slotE = (size_t)(TY + 4) * nx;
+size_t pass_smem(int nx, int TY, int NS, int nz, bool mut, int xs = 1) {
+    const size_t slotE = xs > 1 ? ((size_t)(TY + 4) * nx + 15) / 16 * 16 : (size_t)(TY + 4) * nx;
     const size_t e = (size_t)NS * (2 * slotE + (mut ? (slotE + 1) / 2 : 0)) + 3 * (size_t)(TY + 2) * nx;
     return e * sizeof(double2) + (NS + 2) * 8 + 32 * kNumPartials * 8 + 8 * (size_t)nz + 128;
 }
 
 // Pass tiling: a thread owns `rows` slot rows of one column of the TY + 4 slot rows.
 //   2 rows per thread, <= 512 threads (default);  1 row per thread, <= 512 threads (fallback)
+// Wide rows (nx >= 96) may split each row tile into xs = 2 x parts of ceil(nx / 2) columns plus
+// 2 halo columns per side: the 512-thread / 227 KB limits then allow a taller tile, and the
+// redundant halo work per owned node, (TY + 4) / TY * nxl / (nx / xs), drops (96^3: TY 6 -> 14,
+// 1.67 -> 1.39).  Among the allowed x splits the tiling with the smaller halo factor wins.
 // DOT_CG_TY forces the tile height, DOT_CG_ROWS the rows per thread, DOT_CG_PREFETCH the TMA
-// depth (1..3) -- test knobs.
-CgTiling cg_tiling(int nx, int ny, int nz, int prefetch, int want_ty, int want_rows, bool no_mu) {
-    const bool mut = (nx % 2 == 0) && !no_mu;    // mu in the slots needs 16-byte rows
+// depth (1..3), DOT_CG_XS the x parts -- test knobs.
+CgTiling cg_tiling(int nx, int ny, int nz, int prefetch, int want_ty, int want_rows, bool no_mu, int want_xs) {
     const int NS = std::max(1, std::min(prefetch, 3)) + 2;
     const size_t sm_cta = 227 * 1024;
     struct Opt { int rows, maxt; };
     const Opt opts[2] = {{2, 512}, {1, 512}};
     CgTiling best;
     bool found = false;
-    for (const Opt& o : opts) {
-        if (want_rows > 0 && o.rows != want_rows) continue;
-        int ty = 0;
-        for (int c = 1; c <= ny; ++c) {
-            const int thr = ((c + 4 + o.rows - 1) / o.rows * nx + 31) / 32 * 32;
-            if (thr > o.maxt || pass_smem(nx, c, NS, nz, mut) > sm_cta) break;
-            ty = c;
-            if (want_ty > 0 && c == want_ty) break;
+    double best_cost = 0;
+    for (int xs = 1; xs <= 2; ++xs) {
+        if (want_xs > 0 && xs != want_xs) continue;
+        // x parts of even width (16-byte tensor rows); by default only for 96 <= nx < 128, where it
+        // measured faster (opt96 10-pair batches 0.47 -> 0.53 of the HBM peak); at nx = 128 the
+        // unsplit TY = 4 tile measured faster (0.589 vs 0.561), DESIGN.md "x split"
+        if (xs == 2 && nx % 4 != 0) continue;
+        if (xs == 2 && want_xs != 2 && (nx < 96 || nx >= 128)) continue;
+        const int nxl = xs == 1 ? nx : (nx + 1) / 2 + 4;
+        const bool mut = (nxl % 2 == 0) && (nx % 2 == 0) && !no_mu;    // mu in the slots needs 16-byte rows
+        CgTiling bx;
+        bool fx = false;
+        for (const Opt& o : opts) {
+            if (want_rows > 0 && o.rows != want_rows) continue;
+            int ty = 0;
+            for (int c = 1; c <= ny; ++c) {
+                const int thr = ((c + 4 + o.rows - 1) / o.rows * nxl + 31) / 32 * 32;
+                if (thr > o.maxt || pass_smem(nxl, c, NS, nz, mut, xs) > sm_cta) break;
+                ty = c;
+                if (want_ty > 0 && c == want_ty) break;
+            }
+            if (want_ty > 0 && ty != want_ty) continue;
+            if (ty <= 0) continue;
+            const int nty = (ny + ty - 1) / ty;
+            CgTiling t;
+            t.rows = o.rows;
+            t.TY = (ny + nty - 1) / nty;      // balanced tiles
+            t.nty = (ny + t.TY - 1) / t.TY;
+            t.xs = xs;
+            t.nxl = nxl;
+            t.ntiles = t.nty * xs;
+            t.nslots = NS;
+            t.threads = ((t.TY + 4 + o.rows - 1) / o.rows * nxl + 31) / 32 * 32;
+            t.smem = pass_smem(nxl, t.TY, NS, nz, mut, xs);
+            t.mut = mut;
+            if (!fx || (bx.TY < 4 && t.TY > bx.TY)) {
+                bx = t;
+                fx = true;
+            }
+            if (bx.TY >= 4 || want_ty > 0) break;
         }
-        if (want_ty > 0 && ty != want_ty) continue;
-        if (ty <= 0) continue;
-        const int ntiles = (ny + ty - 1) / ty;
-        CgTiling t;
-        t.rows = o.rows;
-        t.TY = (ny + ntiles - 1) / ntiles;      // balanced tiles
-        t.ntiles = (ny + t.TY - 1) / t.TY;
-        t.nslots = NS;
-        t.threads = ((t.TY + 4 + o.rows - 1) / o.rows * nx + 31) / 32 * 32;
-        t.smem = pass_smem(nx, t.TY, NS, nz, mut);
-        t.mut = mut;
-        if (!found || (best.TY < 4 && t.TY > best.TY)) {
-            best = t;
+        if (!fx) continue;
+        const double cost = (double)(bx.TY + 4) / bx.TY * (double)bx.nxl / ((double)nx / xs);
+        if (!found || cost < best_cost - 1e-9) {
+            best = bx;
+            best_cost = cost;
             found = true;
         }
-        if (best.TY >= 4 || want_ty > 0) break;
     }
     if (!found) throw Error(DOT_ERR_ARG, "no pass tiling fits this grid (nx too large or forced tile height)");
     return best;
@@ -910,18 +982,19 @@ static void launch_pass_ns(const PassArgs& a, int nb, cudaStream_t s) {
     const bool mut = a.tl.mut;
     const bool zc = a.nzch > 1 || a.nzch_tot > 1;
     using KF = void (*)(const PassArgs);
-    KF k = mut ? (zc ? cg_pass_kernel<MAXT, NS, true, RPT, true, 0, 0> : cg_pass_kernel<MAXT, NS, true, RPT, false, 0, 0>)
-               : (zc ? cg_pass_kernel<MAXT, NS, false, RPT, true, 0, 0>
-                     : cg_pass_kernel<MAXT, NS, false, RPT, false, 0, 0>);
+    KF k = mut ? (zc ? cg_pass_kernel<MAXT, NS, true, RPT, true, 0, 0, 0> : cg_pass_kernel<MAXT, NS, true, RPT, false, 0, 0, 0>)
+               : (zc ? cg_pass_kernel<MAXT, NS, false, RPT, true, 0, 0, 0>
+                     : cg_pass_kernel<MAXT, NS, false, RPT, false, 0, 0, 0>);
     // compile-time geometries of the BASELINE grids (default ring depth, 2 rows per thread)
     if constexpr (NS == 4 && RPT == 2) if (mut && !std::getenv("DOT_CG_GENERIC")) {
-#define DOT_GEOM(GX, GT)                                                                         \
-    if (a.op.nx == GX && a.tl.TY == GT)                                                          \
-        k = zc ? cg_pass_kernel<MAXT, NS, true, RPT, true, GX, GT> : cg_pass_kernel<MAXT, NS, true, RPT, false, GX, GT>;
-        DOT_GEOM(32, 16)
-        DOT_GEOM(64, 11)
-        DOT_GEOM(96, 6)
-        DOT_GEOM(128, 4)
+#define DOT_GEOM(GX, GT, GS)                                                                     \
+    if (a.tl.nxl == GX && a.tl.TY == GT && a.tl.xs == GS)                                        \
+        k = zc ? cg_pass_kernel<MAXT, NS, true, RPT, true, GX, GT, GS>                           \
+               : cg_pass_kernel<MAXT, NS, true, RPT, false, GX, GT, GS>;
+        DOT_GEOM(32, 16, 1)
+        DOT_GEOM(64, 11, 1)
+        DOT_GEOM(52, 14, 2)     // 96^3, two x parts
+        DOT_GEOM(128, 4, 1)
 #undef DOT_GEOM
     }
     ensure_smem(k, a.tl.smem);
@@ -938,6 +1011,45 @@ static void launch_pass_r(const PassArgs& a, int nb, cudaStream_t s) {
         case 5: launch_pass_ns<MAXT, 5, RPT>(a, nb, s); break;
         default: throw Error(DOT_ERR_ARG, "pass supports 3..5 ring slots");
     }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        DOT_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) throw Error(DOT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+void set_pass_tmaps(PassArgs& a) {
+    if (a.tl.xs <= 1) return;
+    auto enc = tmap_encoder();
+    const cuuint64_t nx = (cuuint64_t)a.op.nx, ny = (cuuint64_t)a.op.ny, nz = (cuuint64_t)a.op.nz;
+    const cuuint32_t rows = (cuuint32_t)(a.tl.TY + 4), cols = (cuuint32_t)a.tl.nxl;
+    auto check = [](CUresult r) {
+        if (r != CUDA_SUCCESS) throw Error(DOT_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    };
+    const cuuint64_t dim4[4] = {2 * nx, ny, nz, (cuuint64_t)std::max(a.npairs, 1)};
+    const cuuint64_t str4[3] = {2 * nx * 8, 2 * nx * ny * 8, 2 * nx * ny * nz * 8};
+    const cuuint32_t box4[4] = {2 * cols, rows, 1, 1}, es4[4] = {1, 1, 1, 1};
+    for (int i = 0; i < 2; ++i) {
+        check(enc(&a.tmR[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, a.R[i], dim4, str4, box4, es4,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+        check(enc(&a.tmP[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, a.Pv[i], dim4, str4, box4, es4,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+    }
+    if (!a.tl.mut) return;                       // mu is then loaded per thread
+    const cuuint64_t dim3_[3] = {nx, ny, nz};
+    const cuuint64_t str3[2] = {nx * 8, nx * ny * 8};
+    const cuuint32_t box3[3] = {cols, rows, 1}, es3[3] = {1, 1, 1};
+    check(enc(&a.tmMu, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(a.mu), dim3_, str3, box3, es3,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
 }
 
 void set_edge_coefs(PassArgs& a) {

@@ -1,6 +1,8 @@
 // Kernel launchers of the B200 DOT library (internal interface between the
 // C-ABI layer abi.cu and the kernel translation units).
 #pragma once
+#include <cuda.h>
+
 #include "dot_common.cuh"
 
 namespace dot {
@@ -15,11 +17,16 @@ struct CgTiling {
     int rows = 2;         // slot rows per thread (1 or 2)
     bool mut = true;      // mu rides in the ring slots (TMA); else per-thread loads from L2
     int TY = 0, ntiles = 0, nslots = 0, threads = 512;
+    int xs = 1;           // x parts per row tile (wide rows); ntiles = nty * xs CTA tiles
+    int nxl = 0;          // slot row width: nx (xs = 1) or ceil(nx / xs) + 4 (2 halo columns per side)
+    int nty = 0;          // row tiles (sample offsets are per (plane, row tile))
     size_t smem = 0;
 };
 // prefetch: planes loaded ahead (1..3; slots = prefetch + 2); want_ty > 0 forces the tile height,
 // want_rows > 0 the rows per thread
-CgTiling cg_tiling(int nx, int ny, int nz, int prefetch = 2, int want_ty = 0, int want_rows = 0, bool no_mu = false);
+// want_xs > 0 forces the x parts (1 or 2).
+CgTiling cg_tiling(int nx, int ny, int nz, int prefetch = 2, int want_ty = 0, int want_rows = 0, bool no_mu = false,
+                   int want_xs = 0);
 size_t pass_smem(int nx, int TY, int NS, int nz, bool mut);
 
 struct PassArgs {
@@ -50,7 +57,13 @@ struct PassArgs {
     const int32_t* samp_off = nullptr;    // [nz*ntiles+1] ranges of samples per (plane, tile)
     int nP = 0;
     double2* H = nullptr;                 // [hist][npairs][nP] seed residual r_k at the samples
+    // x split (tl.xs > 1): the slot tiles arrive as one tensor copy per vector (rows and columns
+    // outside the domain zero-filled by the copy).  R[i] / Pv[i] as [pair][z][y][2 nx] doubles,
+    // mu as [z][y][nx]; boxes of (TY + 4) rows x nxl columns.  Filled by set_pass_tmaps.
+    CUtensorMap tmR[2], tmP[2], tmMu;
 };
+// encodes PassArgs::tmR / tmP / tmMu from R, Pv, mu, op, tl, npairs (no-op when tl.xs == 1)
+void set_pass_tmaps(PassArgs& a);
 
 struct FoldArgs {
     int k0 = 0, k1 = 0;                   // passes to fold

@@ -460,3 +460,33 @@ def test_segment_gemm_ragged_tiles_and_chunks(dot, monkeypatch, chunk):
     assert rel(Js, Jd) < 1e-12
     Jo = jacobian(prob, wl.p, np.eye(cfg.n_s), np.eye(cfg.n_d))
     assert rel(Js, Jo) < 1e-7
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_x_split_tilings_keep_parity(dot, seed, monkeypatch):
+    """Row tiles split into two x parts (DOT_CG_XS=2: 2 halo columns per side, slot tiles by
+    tensor copies with zero fill outside the domain) on seeded grids with nx = 0 mod 4, ragged
+    row tiles, z chunks and both thread mappings: dense solves and sampled measurements vs
+    the oracle."""
+    rng = np.random.default_rng(2000 + seed)
+    nx = int(rng.choice([8, 12, 20, 28, 36]))
+    ny, nz = int(rng.integers(3, 30)), int(rng.integers(2, 24))
+    monkeypatch.setenv("DOT_CG_XS", "2")
+    monkeypatch.setenv("DOT_CG_ROWS", ["1", "2"][seed % 2])
+    if seed % 3 == 0 and nz >= 8:
+        monkeypatch.setenv("DOT_CG_ZCHUNKS", str(int(rng.integers(2, 5))))
+    L = (float(rng.uniform(1.5, 4.0)), float(rng.uniform(1.5, 4.0)), float(rng.uniform(1.0, 3.0)))
+    cfg = small_config(n=(nx, ny, nz), L=L, src=(2, min(2, ny)), det=(3, min(2, ny)), eps=0.5, seed=seed)
+    prob, wl = small_problem(cfg, with_data=False)
+    g = gpu_problem(dot, cfg, prob, wl)
+    N = prob.grid.N
+    b = rng.standard_normal((2, N)) + 1j * rng.standard_normal((2, N))
+    mu = absorption(wl.p, prob.grid, cfg)
+    for f in range(len(prob.omegas)):
+        x, _ = g.solve(b, f)
+        ref = spla.splu(prob.operator(mu, f).tocsc()).solve(b.T).T
+        assert rel(x, ref) < 1e-11, (nx, ny, nz, f)
+    X = g.solve_sampled(0)
+    samp = g.samples()
+    M = np.transpose(X[:, :, np.searchsorted(samp, wl.det_nodes)], (0, 2, 1))
+    assert rel(M, measurements(prob, wl.p)) < 1e-8, (nx, ny, nz)

@@ -36,7 +36,8 @@ def main():
     gbs = st["pass_bytes"] / max(st["pass_ms"], 1e-9) / 1e6
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     print(f"{name} ncols {ncols}: pass {gbs:.0f} GB/s frac {gbs / peak:.4f} "
-          f"({st['rhs_solved']} solves, {st['pass_ms']:.1f} ms in passes)")
+          f"({st['rhs_solved']} solves, {st['pass_ms']:.1f} ms in passes, "
+          f"{st['rhs_iterations'] / max(st['rhs_solved'], 1):.1f} iterations/solve)")
 
 
 if __name__ == "__main__":
