@@ -122,8 +122,10 @@ def fp64_peak():
     return 40.0, "nominal B200 FP64 tensor 40 TFLOP/s"
 
 
-def ncu_traffic():
-    path = os.path.join(ROOT, "profiles", "cg_pass_traffic.json")
+def ncu_traffic(cfg_name):
+    """DRAM traffic of one captured CG pass launch of this config's grid (tools/make_profiles.py),
+    or None when no capture of that grid is committed."""
+    path = os.path.join(ROOT, "profiles", f"cg_pass_traffic_{cfg_name}.json")
     if os.path.exists(path):
         return json.load(open(path))
     return None
@@ -431,7 +433,7 @@ def main():
                       "shape": list(Lsup.shape) + [Gsup.shape[1]]}
     peak, peak_src = measured_peaks()
     gbs = (st["pass_bytes"] - s0["pass_bytes"]) / max(st["pass_ms"] - s0["pass_ms"], 1e-9) / 1e6
-    traffic = ncu_traffic()
+    traffic = ncu_traffic(cfg.name)
     roof = {"bound": "hbm", "kernel": "cg_pass_kernel", "achieved": gbs, "peak": peak, "unit": "GB/s",
             "frac": gbs / peak, "peak_source": peak_src,
             "algorithmic_bytes": ("32 B per grid point per CG iteration per real seed (read r_k, p_k-1; write "

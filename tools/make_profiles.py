@@ -3,8 +3,8 @@
   python tools/make_profiles.py r01
 writes profiles/<tag>_launches.csv (raw ncu launch list), <tag>_launches_summary.txt
 (per-kernel share of the step), <tag>_ncu_<kernel>.txt (ncu --set full key metrics),
-cocg_pass_traffic.json (DRAM traffic per launch of the COCG pass vs its algorithmic
-bytes; read by bench.py) and <tag>_bench.jsonl (the bench line)."""
+cg_pass_traffic_<config>.json (DRAM traffic per launch of the CG pass vs its algorithmic
+bytes, per captured grid; read by bench.py for that config) and <tag>_bench.jsonl (the bench line)."""
 import collections, csv, json, os, shutil, subprocess, sys
 
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
@@ -46,8 +46,10 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active"]
-traffic = None
-for rep, name in (("prof_pass", "cg_pass"), ("prof_contract", "contract")):
+traffic = {}
+CAPTURES = (("prof_pass", "cg_pass", "full64", 64 ** 3), ("prof_contract", "contract", None, 0),
+            ("prof_pass128", "cg_pass_all128", "all128", 128 ** 3), ("prof_pass96", "cg_pass_opt96", "opt96", 96 ** 3))
+for rep, name, cfgname, npts in CAPTURES:
     path = os.path.join(G, rep + ".ncu-rep")
     if not os.path.exists(path):
         continue
@@ -65,24 +67,26 @@ for rep, name in (("prof_pass", "cg_pass"), ("prof_contract", "contract")):
                      and k.endswith("per_issue_active.ratio") and v[k] not in ("", "n/a")), reverse=True)
         for val, k in st[:8]:
             lines.append(f"  stall {k.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')} = {val:.3f}")
-        if name == "cg_pass" and traffic is None:
+        if cfgname and cfgname not in traffic:
             gx, gy = [int(t) for t in v["Grid Size"].strip("()").split(",")[:2]]
             rd = float(v["dram__bytes_read.sum"]); wr = float(v["dram__bytes_write.sum"])
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             rd *= scale[units[hh.index("dram__bytes_read.sum")]]
             wr *= scale[units[hh.index("dram__bytes_write.sum")]]
-            traffic = {"launch_pairs": gy, "grid": [gx, gy], "dram_bytes": rd + wr,
-                       "algorithmic_bytes_if_all_active": 64.0 * 64 ** 3 * gy,
-                       "note": (f"ncu --set full capture of one cg_pass_kernel launch ({gy} seed pairs, 64^3) in "
-                                f"bench.py --profile: dram read+write per launch vs 32 B/point/seed algorithmic")}
-            traffic["ratio"] = traffic["dram_bytes"] / traffic["algorithmic_bytes_if_all_active"]
+            n = round(npts ** (1 / 3))
+            t = {"config": cfgname, "launch_pairs": gy, "grid": [gx, gy], "dram_bytes": rd + wr,
+                 "algorithmic_bytes_if_all_active": 64.0 * npts * gy,
+                 "note": (f"ncu --set full capture of one cg_pass_kernel launch ({gy} seed pairs, {n}^3): dram "
+                          f"read+write per launch vs 32 B/point/seed algorithmic")}
+            t["ratio"] = t["dram_bytes"] / t["algorithmic_bytes_if_all_active"]
+            traffic[cfgname] = t
     with open(os.path.join(P, f"{tag}_ncu_{name}.txt"), "w") as fo:
         fo.write(f"# ncu --set full --clock-control none --import-source on ({rep}.ncu-rep), bench.py --profile\n")
         fo.write("\n".join(lines) + "\n")
     print("\n".join(lines))
-if traffic:
-    json.dump(traffic, open(os.path.join(P, "cg_pass_traffic.json"), "w"), indent=1)
-    print(traffic)
+for cfgname, t in traffic.items():
+    json.dump(t, open(os.path.join(P, f"cg_pass_traffic_{cfgname}.json"), "w"), indent=1)
+    print(t)
 if os.path.exists(os.path.join(G, "sass_mix.txt")):
     shutil.copy(os.path.join(G, "sass_mix.txt"), os.path.join(P, f"{tag}_ncu_cg_pass_sass_mix.txt"))
 bl = [l for l in open(os.path.join(G, "bench.log")) if l.startswith("{")]
