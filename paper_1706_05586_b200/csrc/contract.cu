@@ -440,6 +440,7 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 //  * seg_tma_gemm_kernel: one producer lane streams the A and B block of each k-tile with one
 //    cp.async.bulk each into a 4-stage ring (full / empty mbarriers); 8 consumer warps (2 per
 //    scheduler), warp tile 16 x 32, run LDS + DMMA only (3 DMMA per fragment pair).
+constexpr int kMaxRbf = 256;                           // bases of one problem (segment GEMM tables)
 namespace tma {
 constexpr int QM = 64, KT = 16, BLK = QM * KT * 24, NST = 4, NCW = 8, NT = 32 * (NCW + 1);
 constexpr size_t SMEM = 128 + (size_t)NST * 2 * BLK;
@@ -514,6 +515,12 @@ __global__ void __launch_bounds__(tma::NT, 1) seg_tma_gemm_kernel(int ld, int ls
     const uint32_t st0 = bar0 + 128;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int per_j = nDT * nn;
+    __shared__ int s_jorder[kMaxRbf], s_kto[kMaxRbf + 1];
+    const int nrbf = nitems / per_j;
+    for (int i = tid; i <= nrbf; i += blockDim.x) {
+        s_kto[i] = kto[i];
+        if (i < nrbf) s_jorder[i] = jorder[i];
+    }
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar0 + 8 * s), "r"(1));
@@ -552,18 +559,23 @@ __global__ void __launch_bounds__(tma::NT, 1) seg_tma_gemm_kernel(int ld, int ls
                 }
                 ++gt;
             };
+            // the next item is claimed one ahead, so the atomic's round trip overlaps the
+            // current item's stages; basis order and k-tile offsets come from registers
+            int it = atomicAdd(counter, 1);
             for (;;) {
-                const int it = atomicAdd(counter, 1);
                 if (it >= nitems) {
                     stage(0, 0, -1, 0, nullptr, nullptr);
                     break;
                 }
-                const int j = jorder[it / per_j], r = it % per_j, ntl = r / nDT, dt = r % nDT;
-                const int g0 = kto[j], nkt = kto[j + 1] - g0;
+                const int nxt = atomicAdd(counter, 1);
+                const int jj = it / per_j, r = it % per_j, ntl = r / nDT, dt = r % nDT;
+                const int j = s_jorder[jj];
+                const int g0 = s_kto[j], nkt = s_kto[j + 1] - g0;
                 const unsigned char* a = Ap + ((size_t)dt * KTn + g0) * BLK;
                 const unsigned char* b = Bp + ((size_t)ntl * KTn + g0) * BLK;
                 if (nkt == 0) stage(0, 0, j, r, nullptr, nullptr);
                 for (int t = 0; t < nkt; ++t) stage(t, nkt, j, r, a + (size_t)t * BLK, b + (size_t)t * BLK);
+                it = nxt;
             }
         }
         return;
@@ -760,7 +772,7 @@ void launch_rbf_segments(const int32_t* F, const int32_t* pos, int K, int n_rbf,
 }
 
 bool contract_seg_applies(int ld, int ls, const GSparse* sp, int n_p) {
-    return sp && sp->seg && sp->n_rbf * 5 == n_p && ld >= 32 && ls >= 8;
+    return sp && sp->seg && sp->n_rbf * 5 == n_p && sp->n_rbf <= kMaxRbf && ld >= 32 && ls >= 8;
 }
 
 void launch_contract_seg(int nb, int T, int ld, int ls, int n_p, int n_rbf, const double2* Lam, size_t lam_bstride,
@@ -821,6 +833,7 @@ void contract_seg_tma(int nb, int T, int ld, int ls, int n_p, const double2* Lam
         return;
     }
     const int KTn = sp.ktiles;
+    if (sp.n_rbf > kMaxRbf) throw Error(DOT_ERR_ARG, "segment GEMM supports up to 256 bases");
     const int nDT = (ld + tma::QM - 1) / tma::QM, nNT = (5 * ls + tma::QM - 1) / tma::QM;
     const size_t per_tile = (size_t)KTn * tma::BLK;
     const size_t set_bytes = (size_t)(nDT + nNT) * per_tile;       // one frequency's A and B tiles
