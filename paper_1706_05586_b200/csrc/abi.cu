@@ -1330,9 +1330,11 @@ int dot_set_params(dot_problem* P, const double* p, int where) {
             P->d_kto = to_device(P, kto.data(), kto.size(), DOT_HOST);
             P->d_ktile = to_device(P, ktile.data(), ktile.size(), DOT_HOST);
             P->d_jorder = to_device(P, jorder.data(), std::max<size_t>(jorder.size(), 1), DOT_HOST);
+            int maxkt = 0;
+            for (int j = 0; j < P->n_rbf; ++j) maxkt = std::max(maxkt, kto[j + 1] - kto[j]);
             P->gsp = GSparse{P->d_seg.get(), P->d_segoff.get(), P->n_rbf, T,
                              reinterpret_cast<const int4*>(P->d_ktile.get()), P->d_kto.get(), kto[P->n_rbf],
-                             P->d_jorder.get()};
+                             P->d_jorder.get(), maxkt};
             P->d_segslot = DBuf<int32_t>(P->arena, std::max(T, 1));
             P->d_Gseg = DBuf<double>(P->arena, 5 * (size_t)std::max(T, 1));
             launch_compose_index(P->d_seg.get(), T, P->d_S_slot.get(), P->d_segslot.get(), s);

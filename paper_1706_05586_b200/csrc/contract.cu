@@ -11,6 +11,7 @@
 // double-buffered in shared memory: the global loads of k-tile t+1 are issued
 // into registers before the DMMAs of tile t and land in the other buffer after
 // them -- one barrier per k-tile.  8 warps, warp w owns rows 16w .. 16w+15.
+#include <array>
 #include <map>
 #include <mutex>
 
@@ -559,15 +560,13 @@ __global__ void __launch_bounds__(tma::NT, 1) seg_tma_gemm_kernel(int ld, int ls
                 }
                 ++gt;
             };
-            // the next item is claimed one ahead, so the atomic's round trip overlaps the
-            // current item's stages; basis order and k-tile offsets come from registers
-            int it = atomicAdd(counter, 1);
+            // (claiming the next item one ahead measured slower: 1.15 vs 1.01 ms at full64)
             for (;;) {
+                const int it = atomicAdd(counter, 1);
                 if (it >= nitems) {
                     stage(0, 0, -1, 0, nullptr, nullptr);
                     break;
                 }
-                const int nxt = atomicAdd(counter, 1);
                 const int jj = it / per_j, r = it % per_j, ntl = r / nDT, dt = r % nDT;
                 const int j = s_jorder[jj];
                 const int g0 = s_kto[j], nkt = s_kto[j + 1] - g0;
@@ -575,7 +574,6 @@ __global__ void __launch_bounds__(tma::NT, 1) seg_tma_gemm_kernel(int ld, int ls
                 const unsigned char* b = Bp + ((size_t)ntl * KTn + g0) * BLK;
                 if (nkt == 0) stage(0, 0, j, r, nullptr, nullptr);
                 for (int t = 0; t < nkt; ++t) stage(t, nkt, j, r, a + (size_t)t * BLK, b + (size_t)t * BLK);
-                it = nxt;
             }
         }
         return;
@@ -653,72 +651,90 @@ __global__ void __launch_bounds__(tma::NT, 1) seg_tma_gemm_kernel(int ld, int ls
 // ---------------------------------------------- small panels: split over the k-tiles
 // The sketched and optimized-direction contractions have ld x ls <= 256 pairs (12 x 12 at
 // the BASELINE configs): a GEMM tile would be mostly padding and 16 bases x n_freq tiles
-// cannot fill 148 SMs.  One CTA per (k-tile of 16 points of one basis, frequency) forms
-// the partial sums of all ld x ls x 5 outputs of that basis over its 16 points (FP64 FMA on
-// shared-memory copies of the fields at those points); a second kernel adds the partials of
-// each basis in k-tile order (deterministic, no atomics) into J.
+// cannot fill 148 SMs.  One CTA per (basis j, chunk of SMALL_KC k-tiles of that basis,
+// frequency) accumulates all ld x ls x 5 outputs of the basis over the chunk's points (FP64
+// FMA on shared-memory copies of the fields, one k-tile at a time); a second kernel adds the
+// chunks of each basis in chunk order (deterministic, no atomics) into J.
 constexpr int SMALL_PAIRS = 256, SMALL_ROWS = 160;   // ld * ls and ld + ls limits of the small form
+constexpr int SMALL_KC = 4;                          // k-tiles per CTA
 
 __global__ void __launch_bounds__(256) contract_small_kernel(int K, int ld, int ls, int n_p,
                                                              const double2* __restrict__ Lam, size_t lam_bs,
                                                              const double2* __restrict__ U, size_t u_bs,
                                                              const double* __restrict__ G,
                                                              const int32_t* __restrict__ seg,
-                                                             const int4* __restrict__ ktile, int KTn,
+                                                             const int4* __restrict__ ktile,
+                                                             const int32_t* __restrict__ kto, int nch,
                                                              double2* __restrict__ part) {
     __shared__ double2 sf[SMALL_ROWS][16];                 // rows [0, ld): Lam, [ld, ld + ls): U
     __shared__ double sg[16][5];
-    const int g = blockIdx.x, f = blockIdx.y;
-    const int4 kt = ktile[g];
-    const int np = min(16, kt.y - kt.x);
+    const int j = blockIdx.x, c = blockIdx.y, f = blockIdx.z;
+    const int g0 = kto[j] + c * SMALL_KC, g1 = min(g0 + SMALL_KC, kto[j + 1]);
+    const int nout = ld * ls * 5;
+    double2* out = part + (((size_t)f * gridDim.x + j) * nch + c) * nout;
+    if (g0 >= g1) {                                        // past this basis's k-tiles: zero chunk
+        for (int o = threadIdx.x; o < nout; o += blockDim.x) out[o] = make_double2(0.0, 0.0);
+        return;
+    }
     const double2* Lf = Lam + (size_t)f * lam_bs;
     const double2* Uf = U + (size_t)f * u_bs;
-    for (int e = threadIdx.x; e < (ld + ls) * 16; e += blockDim.x) {
-        const int r = e >> 4, t = e & 15;
-        double2 v = make_double2(0.0, 0.0);
-        if (t < np) {
-            const int node = seg[kt.x + t];
-            v = r < ld ? Lf[(size_t)r * K + node] : Uf[(size_t)(r - ld) * K + node];
-        }
-        sf[r][t] = v;
-    }
-    if (threadIdx.x < 80) {
-        const int t = threadIdx.x / 5, q = threadIdx.x % 5;
-        sg[t][q] = t < np ? G[(size_t)seg[kt.x + t] * n_p + 5 * kt.z + q] : 0.0;
-    }
-    __syncthreads();
-    const int nout = ld * ls * 5;
-    double2* out = part + ((size_t)f * KTn + g) * nout;
-    for (int o = threadIdx.x; o < nout; o += blockDim.x) {
-        const int q = o % 5, pr = o / 5, d = pr / ls, i = pr - d * ls;
-        double re = 0.0, im = 0.0;
+    constexpr int PER = 8;                                 // outputs per thread kept in registers
+    double re[PER], im[PER];
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-            const double2 h = cmul(sf[d][t], sf[ld + i][t]);
-            re = fma(h.x, sg[t][q], re);
-            im = fma(h.y, sg[t][q], im);
+    for (int u = 0; u < PER; ++u) re[u] = im[u] = 0.0;
+    for (int g = g0; g < g1; ++g) {
+        const int4 kt = ktile[g];
+        const int np = min(16, kt.y - kt.x);
+        __syncthreads();                                   // previous tile consumed
+        for (int e = threadIdx.x; e < (ld + ls) * 16; e += blockDim.x) {
+            const int r = e >> 4, t = e & 15;
+            double2 v = make_double2(0.0, 0.0);
+            if (t < np) {
+                const int node = seg[kt.x + t];
+                v = r < ld ? Lf[(size_t)r * K + node] : Uf[(size_t)(r - ld) * K + node];
+            }
+            sf[r][t] = v;
         }
-        out[o] = make_double2(re, im);
+        if (threadIdx.x < 80) {
+            const int t = threadIdx.x / 5, q = threadIdx.x % 5;
+            sg[t][q] = t < np ? G[(size_t)seg[kt.x + t] * n_p + 5 * j + q] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int o = threadIdx.x + u * blockDim.x;
+            if (o >= nout) break;
+            const int q = o % 5, pr = o / 5, d = pr / ls, i = pr - d * ls;
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+                const double2 h = cmul(sf[d][t], sf[ld + i][t]);
+                re[u] = fma(h.x, sg[t][q], re[u]);
+                im[u] = fma(h.y, sg[t][q], im[u]);
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        const int o = threadIdx.x + u * blockDim.x;
+        if (o < nout) out[o] = make_double2(re[u], im[u]);
     }
 }
 
-__global__ void contract_small_reduce_kernel(int nb, int ld, int ls, int n_p, const double2* __restrict__ part,
-                                             const int32_t* __restrict__ kto, int KTn, double2* J) {
-    const size_t tot = (size_t)nb * ld * ls * n_p;
-    const int nout = ld * ls * 5;
-    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
-        const int k = (int)(e % n_p);
-        const size_t fp = e / n_p;                       // f * npairs + pair
-        const int f = (int)(fp / ((size_t)ld * ls)), pr = (int)(fp % ((size_t)ld * ls));
-        const int j = k / 5, o = pr * 5 + k % 5;
-        double re = 0.0, im = 0.0;
-        for (int g = kto[j]; g < kto[j + 1]; ++g) {
-            const double2 v = part[((size_t)f * KTn + g) * nout + o];
-            re += v.x;
-            im += v.y;
-        }
-        J[e] = make_double2(-re, -im);
+// J[f][pair][5 j + q] = - sum_c part[f][j][c][pair * 5 + q]   (grid: outputs, bases, frequencies)
+__global__ void contract_small_reduce_kernel(int ls, int n_p, int nout, int nch, const double2* __restrict__ part,
+                                             double2* J) {
+    const int j = blockIdx.y, f = blockIdx.z;
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= nout) return;
+    const double2* p = part + ((size_t)f * gridDim.y + j) * nch * nout + o;
+    double re = 0.0, im = 0.0;
+    for (int c = 0; c < nch; ++c) {
+        const double2 v = p[(size_t)c * nout];
+        re += v.x;
+        im += v.y;
     }
+    const int pr = o / 5, q = o % 5;
+    J[((size_t)f * (nout / 5) + pr) * n_p + 5 * j + q] = make_double2(-re, -im);
 }
 
 // Gs[t][q] = G[seg[t]][5 j + q] for the points t of basis j (basis-ordered weights)
@@ -861,8 +877,15 @@ void contract_seg_tma(int nb, int T, int ld, int ls, int n_p, const double2* Lam
         DBuf<int> counters(arena, nb);
         DOT_CUDA_TRY(cudaMemsetAsync(counters.get(), 0, nb * sizeof(int), s));
         cudaStream_t s2 = prescale_stream();
-        cudaEvent_t ev[5];
-        for (auto& e : ev) DOT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        // events of this host thread and device, created once (calls of one thread are ordered)
+        static thread_local std::map<int, std::array<cudaEvent_t, 5>> evs;
+        auto evit = evs.find(dev);
+        if (evit == evs.end()) {
+            std::array<cudaEvent_t, 5> e5;
+            for (auto& e : e5) DOT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            evit = evs.emplace(dev, e5).first;
+        }
+        cudaEvent_t* ev = evit->second.data();
         cudaEvent_t &in_ready = ev[0], *pre = ev + 1, *used = ev + 3;
         DOT_CUDA_TRY(cudaEventRecord(in_ready, s));
         DOT_CUDA_TRY(cudaStreamWaitEvent(s2, in_ready, 0));
@@ -878,7 +901,6 @@ void contract_seg_tma(int nb, int T, int ld, int ls, int n_p, const double2* Lam
             DOT_CUDA_TRY(cudaEventRecord(used[b], s));
             *launches += 2;
         }
-        for (auto& e : ev) DOT_CUDA_TRY(cudaEventDestroy(e));   // released once their work completes
         return;
     }
     // one operand set; B tiles of a frequency in chunks of column tiles when the workspace is short
@@ -910,18 +932,17 @@ void launch_contract(int nb, int K, int ld, int ls, int n_p, const double2* Lam,
         return;
     }
     if (sp && sp->seg && sp->ktile && sp->n_rbf * 5 == n_p && arena && npairs <= SMALL_PAIRS && ld + ls <= SMALL_ROWS) {
-        const int KTn = sp->ktiles;
-        if (KTn == 0) {
+        if (sp->ktiles == 0) {
             DOT_CUDA_TRY(cudaMemsetAsync(J, 0, (size_t)nb * npairs * n_p * sizeof(double2), s));
             return;
         }
-        DBuf<double2> part(*arena, (size_t)nb * KTn * npairs * 5);
-        contract_small_kernel<<<dim3(KTn, nb), 256, 0, s>>>(K, ld, ls, n_p, Lam, lam_bstride, U, u_bstride, G, sp->seg,
-                                                           sp->ktile, KTn, part.get());
+        const int nch = (sp->maxkt + SMALL_KC - 1) / SMALL_KC, nout = npairs * 5;
+        DBuf<double2> part(*arena, (size_t)nb * sp->n_rbf * nch * nout);
+        contract_small_kernel<<<dim3(sp->n_rbf, nch, nb), 256, 0, s>>>(K, ld, ls, n_p, Lam, lam_bstride, U, u_bstride,
+                                                                      G, sp->seg, sp->ktile, sp->kto, nch, part.get());
         DOT_CUDA_TRY(cudaGetLastError());
-        const size_t tot = (size_t)nb * npairs * n_p;
-        contract_small_reduce_kernel<<<(unsigned)std::min<size_t>((tot + 255) / 256, 4096), 256, 0, s>>>(
-            nb, ld, ls, n_p, part.get(), sp->kto, KTn, J);
+        contract_small_reduce_kernel<<<dim3((nout + 127) / 128, sp->n_rbf, nb), 128, 0, s>>>(ls, n_p, nout, nch,
+                                                                                           part.get(), J);
         DOT_CUDA_TRY(cudaGetLastError());
         if (launches) *launches += 2;
         return;

@@ -143,6 +143,7 @@ struct GSparse {
     const int32_t* kto = nullptr;      // [n_rbf + 1]
     int ktiles = 0;                    // kto[n_rbf]
     const int32_t* jorder = nullptr;   // [n_rbf] bases by decreasing k-tile count (work order)
+    int maxkt = 0;                     // largest k-tile count of one basis
 };
 // sp == null (or no segments): dense DMMA contraction over all K points; else the
 // block-sparse one (per basis j, its support points only).
