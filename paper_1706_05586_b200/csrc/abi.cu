@@ -1395,15 +1395,9 @@ int dot_misfit(dot_problem* P, const double* W, int32_t ls, const double* V, int
     DOT_API_END(P)
 }
 
-// block-sparse segment GEMM of basis-ordered panels (DOT_SEG_V1: the round-2a kernel, A/B only)
+// block-sparse segment GEMM of basis-ordered panels
 static void contract_seg(dot_problem* P, int nf, int T, int ld, int ls, const double2* L, size_t lbs, const double2* U,
                          size_t ubs, double2* J) {
-    static const bool v1 = std::getenv("DOT_SEG_V1") != nullptr;
-    if (v1) {
-        launch_contract_seg(nf, T, ld, ls, P->n_p, P->n_rbf, L, lbs, U, ubs, P->d_Gseg.get(), P->gsp.segoff, J,
-                            P->stream);
-        return;
-    }
     contract_seg_tma(nf, T, ld, ls, P->n_p, L, lbs, U, ubs, P->d_Gseg.get(), P->gsp, J, P->arena, P->stream,
                      &P->stats.kernel_launches);
 }

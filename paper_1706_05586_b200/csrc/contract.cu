@@ -269,21 +269,6 @@ __global__ void __launch_bounds__(THREADS) contract_sparse_kernel(int K, int ld,
     }
 }
 
-// ------------------------------------- block-sparse GEMM on basis-ordered panels (default)
-// The support fields are gathered once per call in BASIS order: panel column t of basis j
-// (segoff[j] <= t < segoff[j+1]) is support point seg[t] (only the nonzero
-// components of dA/dp_k enter).  Per (frequency, basis) one complex GEMM with CONTIGUOUS k:
-//     J[d][(q, i)] = - sum_{t in basis j} Lam[d][t] * (Gs[t][q] U[i][t]),   q < 5,
-// M = ld, N = 5 ls.  Tiles 64 x 64, k-tiles of 16, a 3-stage cp.async pipeline (16-byte
-// copies, zero fill past the panel), and the 3-multiply complex product
-//     P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi);  re = P1 - P2, im = P3 - P1 - P2
-// (3 DMMA per fragment instead of 4).  B = Gs * U is formed in the fragment load.
-// Warp w: rows 16 (w & 3) .. +16, columns 32 (w >> 2) .. +32.
-// QRS: padded row stride in double2; QRS = 4 (mod 8) makes every 8-lane phase of a fragment
-// load (2 rows x 4 k) hit 8 distinct 16-byte bank groups (conflict-free LDS.128).
-constexpr int QM = 64, QN = 64, QK = 16, QRS = QK + 4, QST = 3;
-constexpr size_t kSegStage = (size_t)(QM + QN) * QRS * sizeof(double2) + QK * 5 * sizeof(double);
-
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
     const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
@@ -293,126 +278,6 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
 }
 
-__global__ void __launch_bounds__(THREADS, 1) contract_seg_kernel(int T, int ld, int ls, int n_rbf,
-                                                                 const double2* __restrict__ Lam, size_t lam_bs,
-                                                                 const double2* __restrict__ U, size_t u_bs,
-                                                                 const double* __restrict__ Gs,
-                                                                 const int32_t* __restrict__ segoff, int n_p,
-                                                                 double2* J) {
-    extern __shared__ __align__(16) unsigned char qsm[];
-    auto stA = [&](int st) { return reinterpret_cast<double2*>(qsm + st * kSegStage); };
-    auto stU = [&](int st) { return stA(st) + QM * QRS; };
-    auto stG = [&](int st) { return reinterpret_cast<double*>(stU(st) + QN * QRS); };
-    const int f = blockIdx.z / n_rbf, jb = blockIdx.z % n_rbf;
-    const int d0 = blockIdx.x * QM, n0 = blockIdx.y * QN;
-    const int N5 = 5 * ls;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;
-    const double2* Lf = Lam + (size_t)f * lam_bs;
-    const double2* Uf = U + (size_t)f * u_bs;
-    const int s0 = segoff[jb], s1 = segoff[jb + 1];
-    const int nkt = (s1 - s0 + QK - 1) / QK;
-    // loader: 4 A and 4 U elements per thread per k-tile (row = idx / 16, kk = idx % 16)
-    const double2* asrc[4];
-    const double2* usrc[4];
-    bool aok[4], uok[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        const int idx = threadIdx.x + e * THREADS, row = idx / QK;
-        const int d = d0 + row, n = n0 + row;
-        aok[e] = d < ld;
-        uok[e] = n < N5;
-        const int q = uok[e] ? n / ls : 0, i = uok[e] ? n - q * ls : 0;
-        asrc[e] = Lf + (size_t)(aok[e] ? d : 0) * T + s0 + (idx % QK);
-        usrc[e] = Uf + (size_t)i * T + s0 + (idx % QK);
-    }
-    auto load = [&](int kt, int st) {          // k-tile kt (0-based within the basis) -> stage st
-        const int k0 = kt * QK;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int idx = threadIdx.x + e * THREADS, row = idx / QK, kk = idx % QK;
-            const bool kin = s0 + k0 + kk < s1;
-            cp_async16(stA(st) + row * QRS + kk, kin && aok[e] ? asrc[e] + k0 : Lf, kin && aok[e]);
-            cp_async16(stU(st) + row * QRS + kk, kin && uok[e] ? usrc[e] + k0 : Uf, kin && uok[e]);
-        }
-        if (threadIdx.x < QK * 5) {            // the weights ride in the same async group (no
-            const int t = s0 + k0 + threadIdx.x / 5;    // synchronous global load per k-tile)
-            cp_async8(stG(st) + threadIdx.x, t < s1 ? Gs + (size_t)s0 * 5 + k0 * 5 + threadIdx.x : Gs, t < s1);
-        }
-    };
-    // per-thread fragment columns: n = wn + ni*8 + lane/4 -> parameter q of that column
-    int qn[4];
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-        const int n = n0 + wn + ni * 8 + (lane >> 2);
-        qn[ni] = n < N5 ? n / ls : 0;
-    }
-    double p1[2][4][2], p2[2][4][2], p3[2][4][2];
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) p1[mi][ni][h] = p2[mi][ni][h] = p3[mi][ni][h] = 0.0;
-#pragma unroll
-    for (int st = 0; st < QST - 1; ++st) {
-        if (st < nkt) load(st, st);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    }
-    for (int kt = 0; kt < nkt; ++kt) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(QST - 2) : "memory");
-        __syncthreads();                       // stage kt landed (and the G tile stores)
-        const int st = kt % QST;
-        if (kt + QST - 1 < nkt) load(kt + QST - 1, (kt + QST - 1) % QST);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        const double2* A = stA(st);
-        const double2* Ub = stU(st);
-        const double* Gt = stG(st);
-#pragma unroll
-        for (int k4 = 0; k4 < QK; k4 += 4) {
-            const int kk = k4 + (lane & 3);
-            double ar[2], ai[2], as[2];
-#pragma unroll
-            for (int mi = 0; mi < 2; ++mi) {
-                const double2 a = A[(wm + mi * 8 + (lane >> 2)) * QRS + kk];
-                ar[mi] = a.x;
-                ai[mi] = a.y;
-                as[mi] = a.x + a.y;
-            }
-#pragma unroll
-            for (int ni = 0; ni < 4; ++ni) {
-                const double2 u = Ub[(wn + ni * 8 + (lane >> 2)) * QRS + kk];
-                const double g = Gt[kk * 5 + qn[ni]];
-                const double br = g * u.x, bi = g * u.y, bs = br + bi;
-#pragma unroll
-                for (int mi = 0; mi < 2; ++mi) {
-                    dmma(p1[mi][ni][0], p1[mi][ni][1], ar[mi], br);
-                    dmma(p2[mi][ni][0], p2[mi][ni][1], ai[mi], bi);
-                    dmma(p3[mi][ni][0], p3[mi][ni][1], as[mi], bs);
-                }
-            }
-        }
-    }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    // epilogue: J[f][(d, i)][5 jb + q] = -C[d][(q, i)]
-    const int npairs = ld * ls;
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi) {
-        const int d = d0 + wm + mi * 8 + (lane >> 2);
-        if (d >= ld) continue;
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int n = n0 + wn + ni * 8 + 2 * (lane & 3) + h;
-                if (n >= N5) continue;
-                const int q = n / ls, i = n - q * ls;
-                const double re = p1[mi][ni][h] - p2[mi][ni][h];
-                const double im = p3[mi][ni][h] - p1[mi][ni][h] - p2[mi][ni][h];
-                J[((size_t)f * npairs + (size_t)d * ls + i) * n_p + 5 * jb + q] = make_double2(-re, -im);
-            }
-    }
-}
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
@@ -791,21 +656,6 @@ bool contract_seg_applies(int ld, int ls, const GSparse* sp, int n_p) {
     return sp && sp->seg && sp->n_rbf * 5 == n_p && sp->n_rbf <= kMaxRbf && ld >= 32 && ls >= 8;
 }
 
-void launch_contract_seg(int nb, int T, int ld, int ls, int n_p, int n_rbf, const double2* Lam, size_t lam_bstride,
-                         const double2* U, size_t u_bstride, const double* Gs, const int32_t* segoff, double2* J,
-                         cudaStream_t s) {
-    if (nb <= 0 || ld <= 0 || ls <= 0) return;
-    if (T <= 0) {
-        DOT_CUDA_TRY(cudaMemsetAsync(J, 0, (size_t)nb * ld * ls * n_p * sizeof(double2), s));
-        return;
-    }
-    dim3 grid((ld + QM - 1) / QM, (5 * ls + QN - 1) / QN, n_rbf * nb);
-    const size_t smem = QST * kSegStage;
-    ensure_smem(contract_seg_kernel, smem);
-    contract_seg_kernel<<<grid, THREADS, smem, s>>>(T, ld, ls, n_rbf, Lam, lam_bstride, U, u_bstride, Gs, segoff,
-                                                      n_p, J);
-    DOT_CUDA_TRY(cudaGetLastError());
-}
 
 void launch_seg_weights(const double* G, int n_p, const GSparse& sp, double* Gs, cudaStream_t s) {
     if (sp.total <= 0) return;

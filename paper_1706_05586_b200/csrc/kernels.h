@@ -158,10 +158,7 @@ void launch_contract(int nb, int K, int ld, int ls, int n_p, const double2* Lam,
 // U [nb][ls][T] with column t the support point seg[t] of basis j (segoff[j] <= t < segoff[j+1]),
 // Gs [T][5] the basis's weights there.  contract_seg_applies: the panel shape takes this path.
 bool contract_seg_applies(int ld, int ls, const GSparse* sp, int n_p);
-void launch_contract_seg(int nb, int T, int ld, int ls, int n_p, int n_rbf, const double2* Lam, size_t lam_bstride,
-                         const double2* U, size_t u_bstride, const double* Gs, const int32_t* segoff, double2* J,
-                         cudaStream_t s);
-// The same GEMM through pre-formed operand tiles (default): per frequency, a prescale pass
+// The GEMM runs through pre-formed operand tiles: per frequency, a prescale pass
 // writes the 3-multiply operands (A = Lam, B = Gs U as (re, im) + (re + im) planes) as
 // 64-row x 16-point blocks in the exact shared-memory image the GEMM consumes; the GEMM
 // streams them with one cp.async.bulk per block into a 4-stage mbarrier ring and runs LDS +
