@@ -468,8 +468,16 @@ def main():
                      "support_K": st["support_K"], "flops_per_step": (st["contract_flops"] - s0["contract_flops"]) / args.steps,
                      "ms_per_step": (st["contract_ms"] - s0["contract_ms"]) / args.steps,
                      "dense_equivalent_tflops": st["contract_flops_dense"] / max(st["contract_ms"], 1e-9) / 1e9,
+                     # executed DMMA flops of the segment GEMM (3 real products per complex one, padded
+                     # tiles included) over the whole contraction time (prescale and small panels too):
+                     # a lower bound of the FP64 tensor-pipe utilisation
+                     "dmma_executed_tflops": (st["contract_dmma_flops"] - s0["contract_dmma_flops"])
+                     / max(st["contract_ms"] - s0["contract_ms"], 1e-9) / 1e9,
+                     "dmma_executed_frac": (st["contract_dmma_flops"] - s0["contract_dmma_flops"])
+                     / max(st["contract_ms"] - s0["contract_ms"], 1e-9) / 1e9 / fpk,
                      "note": ("block-sparse by basis (PAPER.md L972): useful flops = 4 per (pair, point, parameter) "
-                              "with a nonzero dA/dp block; dense_equivalent counts the K x n_p GEMM it replaces")},
+                              "with a nonzero dA/dp block (the 3-multiply complex GEMM executes 6, so frac <= 0.70); "
+                              "dense_equivalent counts the K x n_p GEMM it replaces")},
         "cpu_baseline": cpu,
         "solver": "multi-shift CG: one real seed per (source|detector) column serves all n_freq frequencies",
         "e2e": e2e,

@@ -94,6 +94,9 @@ typedef struct dot_stats {
     double contract_flops_dense; /* the dense-equivalent flops 4 x pairs x K x n_p of the same calls */
     int64_t seeds_solved;        /* real multi-shift CG seeds run (one serves every frequency)   */
     int64_t seed_iterations;     /* sum over seeds of their iterations                           */
+    double contract_dmma_flops;  /* FP64 tensor (DMMA) flops the segment GEMM executed: 3 real
+                                    products per complex one, padded tiles included (the useful
+                                    flops above are 2/3 of it at most)                           */
 } dot_stats;
 
 const char* dot_version(void);

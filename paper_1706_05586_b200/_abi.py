@@ -43,6 +43,7 @@ class DotStats(C.Structure):
         ("support_K", C.c_int32), ("n_samples", C.c_int32),
         ("contract_flops_dense", C.c_double),
         ("seeds_solved", C.c_int64), ("seed_iterations", C.c_int64),
+        ("contract_dmma_flops", C.c_double),
     ]
 
     def as_dict(self):

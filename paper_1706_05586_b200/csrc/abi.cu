@@ -1399,7 +1399,7 @@ int dot_misfit(dot_problem* P, const double* W, int32_t ls, const double* V, int
 static void contract_seg(dot_problem* P, int nf, int T, int ld, int ls, const double2* L, size_t lbs, const double2* U,
                          size_t ubs, double2* J) {
     contract_seg_tma(nf, T, ld, ls, P->n_p, L, lbs, U, ubs, P->d_Gseg.get(), P->gsp, J, P->arena, P->stream,
-                     &P->stats.kernel_launches);
+                     &P->stats.kernel_launches, &P->stats.contract_dmma_flops);
 }
 
 int dot_jacobian(dot_problem* P, const double* W, int32_t ls, const double* V, int32_t ld, int where,

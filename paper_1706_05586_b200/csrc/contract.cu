@@ -691,7 +691,7 @@ static cudaStream_t prescale_stream() {
 
 void contract_seg_tma(int nb, int T, int ld, int ls, int n_p, const double2* Lam, size_t lam_bstride,
                       const double2* U, size_t u_bstride, const double* Gs, const GSparse& sp, double2* J,
-                      Arena& arena, cudaStream_t s, int64_t* launches) {
+                      Arena& arena, cudaStream_t s, int64_t* launches, double* dmma_flops) {
     if (nb <= 0 || ld <= 0 || ls <= 0) return;
     const int npairs = ld * ls;
     if (T <= 0 || sp.ktiles <= 0) {
@@ -703,6 +703,8 @@ void contract_seg_tma(int nb, int T, int ld, int ls, int n_p, const double2* Lam
     const int nDT = (ld + tma::QM - 1) / tma::QM, nNT = (5 * ls + tma::QM - 1) / tma::QM;
     const size_t per_tile = (size_t)KTn * tma::BLK;
     const size_t set_bytes = (size_t)(nDT + nNT) * per_tile;       // one frequency's A and B tiles
+    // executed DMMA flops: per (item, k-tile) 3 products of 64 x 64 x 16 real multiply-adds
+    if (dmma_flops) *dmma_flops += (double)nb * KTn * nDT * nNT * 3.0 * 2.0 * tma::QM * tma::QM * tma::KT;
     ensure_smem(seg_tma_gemm_kernel, tma::SMEM);
     int sms = 0, dev = 0;
     DOT_CUDA_TRY(cudaGetDevice(&dev));

@@ -166,7 +166,7 @@ bool contract_seg_applies(int ld, int ls, const GSparse* sp, int n_p);
 // launches are added to *launches.
 void contract_seg_tma(int nb, int T, int ld, int ls, int n_p, const double2* Lam, size_t lam_bstride,
                       const double2* U, size_t u_bstride, const double* Gs, const GSparse& sp, double2* J,
-                      Arena& arena, cudaStream_t s, int64_t* launches);
+                      Arena& arena, cudaStream_t s, int64_t* launches, double* dmma_flops = nullptr);
 // bytes of one frequency's operand tiles (the workspace estimate)
 size_t contract_seg_tma_bytes(int ld, int ls, long long total, int n_rbf);
 // Gs[t][q] = G[seg[t]][5 j + q]
