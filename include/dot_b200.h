@@ -151,7 +151,12 @@ int dot_misfit(dot_problem* P, const double* W, int32_t ls, const double* V, int
  * (Eqs. (2.8), (3.12), (Jacobian kth column) L966-972).  Forward fields
  * come from the cache of a preceding dot_misfit/dot_jacobian with the same W (or
  * by linear combination of cached full-data fields), else are solved; the ld
- * adjoint solves likewise.  The contraction runs on FP64 tensor cores (DMMA). */
+ * adjoint solves likewise.  The contraction is block-sparse by basis (L972: only the
+ * points where dA/dp_k != 0 enter): panels of ld >= 32 rows and ls >= 8 columns run as a
+ * 3-multiply complex GEMM per (frequency, basis) on FP64 tensor cores (DMMA); small sketched
+ * panels (ld * ls <= 256) as FP64 FMA partial sums over k-tiles with a fixed-order reduction.
+ * Scratch (operand tiles, partials) comes from the bound workspace: DOT_ERR_WORKSPACE if
+ * it cannot hold one frequency's operand tiles for one column tile. */
 int dot_jacobian(dot_problem* P, const double* W, int32_t ls, const double* V, int32_t ld,
                  int where, double* J_out);
 
