@@ -757,8 +757,8 @@ void contract_seg_tma(int nb, int T, int ld, int ls, int n_p, const double2* Lam
     }
     // one operand set; B tiles of a frequency in chunks of column tiles when the workspace is short
     DBuf<unsigned char> Ap(arena, nDT * per_tile);
-    const size_t room = arena.largest_free();
-    int chunk = (int)std::max<size_t>(1, std::min<size_t>(nNT, room > per_tile ? room / per_tile : 1));
+    const size_t room = arena.largest_free(), margin = (size_t)1 << 20;     // margin: the counters
+    int chunk = (int)std::max<size_t>(1, std::min<size_t>(nNT, room > per_tile + margin ? (room - margin) / per_tile : 1));
     if (chunk_env) chunk = std::max(1, std::min(chunk, std::atoi(std::getenv("DOT_SEG_CHUNK"))));
     DBuf<unsigned char> Bp(arena, (size_t)chunk * per_tile);
     const int nch = (nNT + chunk - 1) / chunk;
