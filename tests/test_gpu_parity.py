@@ -490,3 +490,24 @@ def test_x_split_tilings_keep_parity(dot, seed, monkeypatch):
     samp = g.samples()
     M = np.transpose(X[:, :, np.searchsorted(samp, wl.det_nodes)], (0, 2, 1))
     assert rel(M, measurements(prob, wl.p)) < 1e-8, (nx, ny, nz)
+
+
+def test_contraction_with_a_basis_without_support_points(dot):
+    """A basis whose centre lies far outside the domain has dA/dp = 0 everywhere (no points
+    in its segment): the segment GEMM's items of that basis and the small-panel chunks are
+    empty and its five J columns are exactly zero; the other columns match the oracle."""
+    cfg = small_config(n=(24, 20, 10), L=(4.0, 3.5, 2.5), src=(3, 3), det=(8, 5), n_rbf=4, eps=0.5)
+    prob, wl = small_problem(cfg)
+    wl.p[5 * 3 + 2: 5 * 3 + 5] = 100.0                    # basis 3: centre far outside
+    g = gpu_problem(dot, cfg, prob, wl)
+    J = g.jacobian(None, None)                            # ld = 40, ls = 9: the segment GEMM
+    assert np.all(J[..., 15:20] == 0)
+    Jo = jacobian(prob, wl.p, np.eye(cfg.n_s), np.eye(cfg.n_d))
+    assert np.abs(Jo[..., 15:20]).max() == 0
+    assert rel(J, Jo) < 1e-7
+    rng = np.random.default_rng(8)
+    W = np.sign(rng.standard_normal((cfg.n_s, 3)))
+    V = np.sign(rng.standard_normal((cfg.n_d, 4)))
+    Js = g.jacobian(W, V)                                 # 4 x 3 pairs: the small-panel form
+    assert np.all(Js[..., 15:20] == 0)
+    assert rel(Js, jacobian(prob, wl.p, W, V)) < 1e-7
