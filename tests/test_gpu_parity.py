@@ -511,3 +511,20 @@ def test_contraction_with_a_basis_without_support_points(dot):
     Js = g.jacobian(W, V)                                 # 4 x 3 pairs: the small-panel form
     assert np.all(Js[..., 15:20] == 0)
     assert rel(Js, jacobian(prob, wl.p, W, V)) < 1e-7
+
+
+def test_mid_size_sketched_panels_take_the_gathered_kernel(dot):
+    """Sketched panels too wide for the small form (ld x ls = 400 > 256) and too narrow for
+    the segment GEMM (ld < 32) run the S-ordered block-sparse kernel: oracle parity."""
+    cfg = small_config(n=(24, 20, 10), L=(4.0, 3.5, 2.5), src=(3, 3), det=(8, 5), n_rbf=4, eps=0.5)
+    prob, wl = small_problem(cfg)
+    g = gpu_problem(dot, cfg, prob, wl)
+    rng = np.random.default_rng(9)
+    W = np.sign(rng.standard_normal((cfg.n_s, 20)))
+    V = np.sign(rng.standard_normal((cfg.n_d, 20)))
+    g.reset_stats()
+    J = g.jacobian(W, V)
+    st = g.stats()
+    assert st["contract_flops"] < st["contract_flops_dense"]      # block-sparse
+    assert st["contract_dmma_flops"] == 0                          # not the segment GEMM
+    assert rel(J, jacobian(prob, wl.p, W, V)) < 1e-7
