@@ -444,6 +444,19 @@ def main():
             "traffic_note": traffic["note"] if traffic else "no ncu --set full capture committed yet"}
     jf = st["contract_flops"] / max(st["contract_ms"], 1e-9) / 1e9
     fpk, fsrc = fp64_peak()
+
+    def gemm_line(st, s0, steps, fpk):
+        gms = st["gemm_ms"] - s0["gemm_ms"]
+        if gms <= 0:
+            return None
+        gfl = st["gemm_flops"] - s0["gemm_flops"]
+        dmma = st["contract_dmma_flops"] - s0["contract_dmma_flops"]
+        return {"what": "full-data Jacobian calls (prescale + segment GEMM, CUDA events on the library stream)",
+                "achieved_tflops": gfl / gms / 1e9, "frac": gfl / gms / 1e9 / fpk,
+                "ms_per_step": gms / steps, "flops_per_step": gfl / steps,
+                "dmma_executed_tflops": dmma / gms / 1e9, "dmma_executed_frac": dmma / gms / 1e9 / fpk,
+                "small_panel_ms_per_step": (st["contract_ms"] - s0["contract_ms"] - gms) / steps}
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -475,6 +488,9 @@ def main():
                      / max(st["contract_ms"] - s0["contract_ms"], 1e-9) / 1e9,
                      "dmma_executed_frac": (st["contract_dmma_flops"] - s0["contract_dmma_flops"])
                      / max(st["contract_ms"] - s0["contract_ms"], 1e-9) / 1e9 / fpk,
+                     # the segment-GEMM calls alone (large panels: the full-data Jacobian), apart from
+                     # the small-panel sketched / optimized-direction contractions (few flops, latency-bound)
+                     "gemm": gemm_line(st, s0, args.steps, fpk),
                      "note": ("block-sparse by basis (PAPER.md L972): useful flops = 4 per (pair, point, parameter) "
                               "with a nonzero dA/dp block (the 3-multiply complex GEMM executes 6, so frac <= 0.70); "
                               "dense_equivalent counts the K x n_p GEMM it replaces")},

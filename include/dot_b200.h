@@ -97,6 +97,9 @@ typedef struct dot_stats {
     double contract_dmma_flops;  /* FP64 tensor (DMMA) flops the segment GEMM executed: 3 real
                                     products per complex one, padded tiles included (the useful
                                     flops above are 2/3 of it at most)                           */
+    double gemm_ms;              /* the part of contract_ms spent in calls that took the segment
+                                    GEMM path (large panels: the full-data Jacobian)            */
+    double gemm_flops;           /* the useful flops of those calls (part of contract_flops)   */
 } dot_stats;
 
 const char* dot_version(void);

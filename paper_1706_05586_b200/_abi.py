@@ -44,6 +44,7 @@ class DotStats(C.Structure):
         ("contract_flops_dense", C.c_double),
         ("seeds_solved", C.c_int64), ("seed_iterations", C.c_int64),
         ("contract_dmma_flops", C.c_double),
+        ("gemm_ms", C.c_double), ("gemm_flops", C.c_double),
     ]
 
     def as_dict(self):

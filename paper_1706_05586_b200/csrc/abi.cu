@@ -1449,10 +1449,12 @@ int dot_jacobian(dot_problem* P, const double* W, int32_t ls, const double* V, i
         float ms = 0;
         DOT_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
         P->stats.contract_ms += ms;
+        if (seg) P->stats.gemm_ms += ms;
     }
     // useful flops: 4 per (pair, point, parameter) with a nonzero weight block (5 per basis
     // over its points when the block-sparse kernel runs; the dense K x n_p otherwise)
     P->stats.contract_flops += 4.0 * nf * ld * ls * (P->gsp.seg ? 5.0 * (double)P->gsp.total : (double)K * P->n_p);
+    if (seg) P->stats.gemm_flops += 4.0 * nf * ld * ls * 5.0 * (double)P->gsp.total;
     P->stats.contract_flops_dense += 4.0 * nf * ld * ls * (double)K * P->n_p;
     if (where == DOT_HOST) {
         DOT_CUDA_TRY(cudaMemcpyAsync(J_out, J, nJ * sizeof(double2), cudaMemcpyDeviceToHost, s));
@@ -1817,7 +1819,8 @@ int dot_contract_fields(dot_problem* P, int32_t ld, int32_t ls, const double* La
             DOT_CUDA_TRY(cudaEventRecord(e0, s));
         }
     };
-    if (contract_seg_applies(ld, ls, &P->gsp, P->n_p)) {
+    const bool segp = contract_seg_applies(ld, ls, &P->gsp, P->n_p);
+    if (segp) {
         // reorder the S-ordered panels into basis order (one gather), then the segment GEMM
         const int T = (int)P->gsp.total;
         DBuf<double2> Lg(P->arena, std::max<size_t>((size_t)nf * ld * T, 1)), Ug(P->arena, std::max<size_t>((size_t)nf * ls * T, 1));
@@ -1840,8 +1843,10 @@ int dot_contract_fields(dot_problem* P, int32_t ld, int32_t ls, const double* La
         float ms = 0;
         DOT_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
         P->stats.contract_ms += ms;
+        if (segp) P->stats.gemm_ms += ms;
     }
     P->stats.contract_flops += 4.0 * nf * ld * ls * (P->gsp.seg ? 5.0 * (double)P->gsp.total : (double)K * P->n_p);
+    if (segp) P->stats.gemm_flops += 4.0 * nf * ld * ls * 5.0 * (double)P->gsp.total;
     P->stats.contract_flops_dense += 4.0 * nf * ld * ls * (double)K * P->n_p;
     DOT_API_END(P)
 }
