@@ -72,8 +72,15 @@ struct dot_problem {
     int* h_count = nullptr;          // [2] pinned, pipelined convergence polls
     cudaEvent_t poll_ev[2] = {nullptr, nullptr};
     int num_sms = 148;
+    // second stream of the pass groups (half of a multi-wave batch runs there, so one half's
+    // wave tail is filled by the other half's CTAs) and its fork / join events
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
 
     ~dot_problem() {
+        if (fork_ev) cudaEventDestroy(fork_ev);
+        if (join_ev) cudaEventDestroy(join_ev);
+        if (side) cudaStreamDestroy(side);
         for (auto e : events) cudaEventDestroy(e);
         for (auto e : poll_ev)
             if (e) cudaEventDestroy(e);
@@ -365,11 +372,39 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, c
         size_t ev = 0;
         for (;;) {
             if (P->timing) DOT_CUDA_TRY(cudaEventRecord(event_at(P, ev++), P->stream));
+            // a batch of two or more waves runs as two half batches on two streams: pass k of
+            // one half fills the SMs the other half's wave tail leaves idle (the halves are
+            // independent seeds; they join before the fold / convergence count of the group)
+            const long long ctas = (long long)P->tl.ntiles * nzch * nb_launch;
+            const bool split = nb_launch >= 2 && ctas >= 2LL * P->num_sms && !std::getenv("DOT_CG_NOSPLIT");
+            const int h = nb_launch / 2;
+            if (split) {
+                if (!P->side) {
+                    DOT_CUDA_TRY(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
+                    DOT_CUDA_TRY(cudaEventCreateWithFlags(&P->fork_ev, cudaEventDisableTiming));
+                    DOT_CUDA_TRY(cudaEventCreateWithFlags(&P->join_ev, cudaEventDisableTiming));
+                }
+                DOT_CUDA_TRY(cudaEventRecord(P->fork_ev, P->stream));
+                DOT_CUDA_TRY(cudaStreamWaitEvent(P->side, P->fork_ev, 0));
+            }
             for (int i = 0; i < CHK; ++i) {
                 a.k = k++;
-                launch_cg_pass(a, nb_launch, P->stream);
+                if (split) {
+                    a.pair0 = 0;
+                    launch_cg_pass(a, h, P->stream);
+                    a.pair0 = h;
+                    launch_cg_pass(a, nb_launch - h, P->side);
+                    a.pair0 = 0;
+                    P->stats.kernel_launches++;
+                } else {
+                    launch_cg_pass(a, nb_launch, P->stream);
+                }
                 P->stats.kernel_launches++;
                 P->stats.pass_launches++;
+            }
+            if (split) {
+                DOT_CUDA_TRY(cudaEventRecord(P->join_ev, P->side));
+                DOT_CUDA_TRY(cudaStreamWaitEvent(P->stream, P->join_ev, 0));
             }
             if (P->timing) DOT_CUDA_TRY(cudaEventRecord(event_at(P, ev++), P->stream));
             if (k - kf >= hist) {
@@ -1508,12 +1543,15 @@ int dot_optimize_directions_subspace(dot_problem* P, int32_t k, int32_t iters, i
     const int nf = P->n_freq, K = P->K, nP = P->nP;
     cudaStream_t s = P->stream;
     SubspaceOps ops;
-    ops.fields = [&](int side, const double* d_coeff, int ncols, double2* out) {
-        DBuf<double2> XP(P->arena, std::max<size_t>((size_t)nf * ncols * nP, 1));
-        solve_batch(P, {Seg{side, d_coeff, ncols}}, nullptr, {}, XP.get(), nf * ncols, nP, P->d_P.get(),
-                    P->d_off.get());
-        launch_gather_cols(nf, ncols, K, XP.get(), (size_t)ncols * nP, nP, P->d_S_slot.get(), out, (size_t)ncols * K,
-                           K, s);
+    ops.fields = [&](int side, const double* d_coeff, int ncols, double2* out, double2* outP) {
+        DBuf<double2> XPt;
+        double2* XP = outP;
+        if (!XP) {
+            XPt = DBuf<double2>(P->arena, std::max<size_t>((size_t)nf * ncols * nP, 1));
+            XP = XPt.get();
+        }
+        solve_batch(P, {Seg{side, d_coeff, ncols}}, nullptr, {}, XP, nf * ncols, nP, P->d_P.get(), P->d_off.get());
+        launch_gather_cols(nf, ncols, K, XP, (size_t)ncols * nP, nP, P->d_S_slot.get(), out, (size_t)ncols * K, K, s);
         P->stats.kernel_launches++;
     };
     ops.solve_support = [&](const double2* w, int nvec, int side, double2* out) {
@@ -1531,6 +1569,35 @@ int dot_optimize_directions_subspace(dot_problem* P, int32_t k, int32_t iters, i
         // b_s^T x = theta_s / (hx hy hz) x[src_s]  (reading R6), on the device
         if (side == 0) launch_scale_cols(out, (size_t)nr, n_side, P->d_src_scale.get(), s);
         P->stats.kernel_launches += side == 0 ? 3 : 2;
+    };
+    ops.start_fields = [&](const std::vector<double>& W0, int l0, const std::vector<double>& V0, int d0, double2* zw,
+                           double2* yv, double2* zwP, double2* yvP) {
+        prefetch_fields(P, {Req{0, W0, false, l0}, Req{1, V0, false, d0}});   // no solves after jacobian(W, V)
+        DBuf<double2> t0, t1;
+        const double2* XZ = get_fields(P, 0, W0, false, l0, t0);
+        const double2* XY = get_fields(P, 1, V0, false, d0, t1);
+        launch_gather_cols(nf, l0, K, XZ, (size_t)l0 * nP, nP, P->d_S_slot.get(), zw, (size_t)l0 * K, K, s);
+        launch_gather_cols(nf, d0, K, XY, (size_t)d0 * nP, nP, P->d_S_slot.get(), yv, (size_t)d0 * K, K, s);
+        DOT_CUDA_TRY(cudaMemcpyAsync(zwP, XZ, (size_t)nf * l0 * nP * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+        DOT_CUDA_TRY(cudaMemcpyAsync(yvP, XY, (size_t)nf * d0 * nP * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+        P->stats.kernel_launches += 2;
+        sync(P);                                       // t0 / t1 are released on return
+    };
+    ops.finish = [&](const std::vector<double>& W1, int a1, DBuf<double2>& zwP, const std::vector<double>& V1, int b1,
+                     DBuf<double2>& yvP) {
+        const std::vector<double>* cf[2] = {&W1, &V1};
+        const int nc[2] = {a1, b1};
+        DBuf<double2>* fb[2] = {&zwP, &yvP};
+        for (int side = 0; side < 2; ++side) {
+            FieldCache& c = P->cache[side];
+            c.blk = std::make_shared<DBuf<double2>>(std::move(*fb[side]));
+            c.X = c.blk->get();
+            c.valid = true;
+            c.identity = false;
+            c.ncols = nc[side];
+            c.coeff = *cf[side];
+            c.sel.clear();
+        }
     };
     OptContext oc{P->arena, P->stream, P->n_freq, P->n_src, P->n_det, P->n_p, P->K, P->nP,
                   nullptr, nullptr, P->d_S_slot.get(), P->d_G.get(), &P->stats.kernel_launches, &P->gsp};

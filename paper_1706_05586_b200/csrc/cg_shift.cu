@@ -251,7 +251,8 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
     constexpr int PD = NS - 2;                          // TMA planes in flight
     const int ntiles = a.tl.ntiles;
     const int tile = blockIdx.x % ntiles, zc = a.zc0 + blockIdx.x / ntiles;
-    const int pair = a.act ? a.act[blockIdx.y] : blockIdx.y;       // active-list compaction (tail passes)
+    const int yrow = a.pair0 + (int)blockIdx.y;                    // split launches: rows [pair0, pair0 + ny)
+    const int pair = a.act ? a.act[yrow] : yrow;                   // active-list compaction (tail passes)
     if (pair < 0) return;                                          // slot past the active count
     // x split (wide rows): tile = (row tile ty, x part xp); the slot rows are nx = the part's
     // xw columns plus 2 halo columns on each side (local column c = global column cx0 + c)

@@ -37,7 +37,8 @@ struct PassArgs {
     int zlen = 0;                 // planes per z chunk
     int zc0 = 0;                  // first (global) z chunk of this launch (z-slab domain decomposition)
     int nzch_tot = 1;             // global z chunks: partial slots per pair = ntiles * nzch_tot
-    const int32_t* act = nullptr; // grid row y iterates pair act[y] (active list), null = identity
+    const int32_t* act = nullptr; // grid row y iterates pair act[pair0 + y] (active list), null = identity
+    int pair0 = 0;                // first grid row of this launch (a batch split over two streams)
     int max_iter = 0;
     double tol2 = 0;              // tol^2
     int nshift = 0;               // frequencies (shifts i omega_f / nu of the scaled system)

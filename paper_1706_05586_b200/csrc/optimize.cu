@@ -337,23 +337,22 @@ double optimize_two_phase(OptContext& c, int k, std::vector<double>& W, int ls, 
 double optimize_two_phase_subspace(OptContext& c, SubspaceOps& ops, int k, int iters, int blk,
                                    std::vector<double>& W, int ls, std::vector<double>& V, int ld,
                                    const std::vector<double>& X0s, const std::vector<double>& X0d) {
-    const int nf = c.nf, ns = c.ns, nd = c.nd, n_p = c.n_p, K = c.K;
+    const int nf = c.nf, ns = c.ns, nd = c.nd, n_p = c.n_p, K = c.K, nP = c.nP;
     cudaStream_t s = c.stream;
     auto sync = [&]() { DOT_CUDA_TRY(cudaStreamSynchronize(s)); };
-    auto fields = [&](int side, const double* d_coeff, int ncols) {     // device coefficients
+    // fields of device coefficients on S ([nf][ncols][K], returned) and on the samples P (outP)
+    auto fields = [&](int side, const double* d_coeff, int ncols, DBuf<double2>& outP) {
         DBuf<double2> out(c.arena, std::max<size_t>((size_t)nf * ncols * K, 1));
-        ops.fields(side, d_coeff, ncols, out.get());
+        outP = DBuf<double2>(c.arena, std::max<size_t>((size_t)nf * ncols * nP, 1));
+        ops.fields(side, d_coeff, ncols, out.get(), outP.get());
         return out;
     };
-    auto fields_h = [&](int side, const std::vector<double>& coeff, int ncols) {
-        DBuf<double> dc(c.arena, std::max<size_t>(coeff.size(), 1));
-        DOT_CUDA_TRY(cudaMemcpyAsync(dc.get(), coeff.data(), coeff.size() * 8, cudaMemcpyHostToDevice, s));
-        DBuf<double2> out = fields(side, dc.get(), ncols);
-        sync();
-        return out;
-    };
-    // z fields of W and y fields of V on S: [nf][cols][K]
-    DBuf<double2> ZW = fields_h(0, W, ls), YV = fields_h(1, V, ld);
+    // z fields of W and y fields of V on S [nf][cols][K] (contractions) and on the samples P
+    // [nf][cols][nP] (kept in step, so that the final W, V leave their fields in the caches)
+    DBuf<double2> ZW(c.arena, std::max<size_t>((size_t)nf * ls * K, 1)), YV(c.arena, std::max<size_t>((size_t)nf * ld * K, 1));
+    DBuf<double2> ZWP(c.arena, std::max<size_t>((size_t)nf * ls * nP, 1)), YVP(c.arena, std::max<size_t>((size_t)nf * ld * nP, 1));
+    ops.start_fields(W, ls, V, ld, ZW.get(), YV.get(), ZWP.get(), YVP.get());
+    sync();
     int a = ls, b = ld;
 
     auto contract = [&](const double2* lam, int nl, const double2* u, int nu) {
@@ -362,12 +361,12 @@ double optimize_two_phase_subspace(OptContext& c, SubspaceOps& ops, int k, int i
                         c.launches);
         return J;
     };
-    // new fields F' [nf][m][K] = sum_j Gam[j][m] F[f][j][K]  (Gam host [ncols][m])
-    auto combine = [&](const DBuf<double2>& F, int ncols, const std::vector<double>& Gam, int m) {
+    // new fields F' [nf][m][L] = sum_j Gam[j][m] F[f][j][L]  (Gam host [ncols][m]; L = K or nP)
+    auto combine = [&](const DBuf<double2>& F, int ncols, const std::vector<double>& Gam, int m, int L) {
         DBuf<double> dG(c.arena, Gam.size());
         DOT_CUDA_TRY(cudaMemcpyAsync(dG.get(), Gam.data(), Gam.size() * 8, cudaMemcpyHostToDevice, s));
-        DBuf<double2> out(c.arena, std::max<size_t>((size_t)nf * m * K, 1));
-        launch_rc_gemm(nf, m, K, ncols, dG.get(), m, F.get(), (size_t)ncols * K, K, 1, out.get(), (size_t)m * K, K, 1, s);
+        DBuf<double2> out(c.arena, std::max<size_t>((size_t)nf * m * L, 1));
+        launch_rc_gemm(nf, m, L, ncols, dG.get(), m, F.get(), (size_t)ncols * L, L, 1, out.get(), (size_t)m * L, L, 1, s);
         *c.launches += 1;
         sync();
         return out;
@@ -401,14 +400,16 @@ double optimize_two_phase_subspace(OptContext& c, SubspaceOps& ops, int k, int i
             DBuf<double2> J = contract(YV.get(), b, ZW.get(), a);
             std::vector<double> Gam = top(gram_of(J, nf * b, a, n_p), a, a - 1);
             W = matmul(W, ns, a, Gam, a - 1);
-            ZW = combine(ZW, a, Gam, a - 1);
+            ZW = combine(ZW, a, Gam, a - 1, K);
+            ZWP = combine(ZWP, a, Gam, a - 1, nP);
             --a;
         }
         {
             DBuf<double2> J = contract(YV.get(), b, ZW.get(), a);
             std::vector<double> Gam = top(gram_of(J, nf, b, a * n_p), b, b - 1);
             V = matmul(V, nd, b, Gam, b - 1);
-            YV = combine(YV, b, Gam, b - 1);
+            YV = combine(YV, b, Gam, b - 1, K);
+            YVP = combine(YVP, b, Gam, b - 1, nP);
             --b;
         }
     }
@@ -421,7 +422,8 @@ double optimize_two_phase_subspace(OptContext& c, SubspaceOps& ops, int k, int i
     DBuf<int> dfail(c.arena, 1);
     DOT_CUDA_TRY(cudaMemsetAsync(dfail.get(), 0, sizeof(int), s));
     auto add_step = [&](int side, std::vector<double>& M, int l, const DBuf<double2>& F, int nF,
-                        const std::vector<double>& X0all, int step, DBuf<double2>& newfield) {
+                        const std::vector<double>& X0all, int step, DBuf<double2>& newfield,
+                        DBuf<double2>& newfieldP) {
         const int n = side == 0 ? ns : nd;
         const std::vector<double> QMh = orth_basis(M, n, l);
         DBuf<double> QM(c.arena, QMh.size()), dQ(c.arena, (size_t)n * blk), dY(c.arena, (size_t)n * blk);
@@ -437,8 +439,8 @@ double optimize_two_phase_subspace(OptContext& c, SubspaceOps& ops, int k, int i
             *c.launches += 1;
         };
         // Y = K Q (Q: n x blk in range(P)); FQ receives the fields of Q on S
-        auto applyK = [&](DBuf<double2>& FQ) {
-            FQ = fields(side, dQ.get(), blk);                               // [nf][blk][K]
+        auto applyK = [&](DBuf<double2>& FQ, DBuf<double2>& FQP) {
+            FQ = fields(side, dQ.get(), blk, FQP);                          // [nf][blk][K], [nf][blk][nP]
             // T[f][..] = Xr^T q in complex form; coefficients C[f][q][i][k] = conj(T)
             DBuf<double2> J = side == 0 ? contract(F.get(), nF, FQ.get(), blk)    // [nf][nF][blk][n_p]
                                         : contract(FQ.get(), blk, F.get(), nF);   // [nf][blk][nF][n_p]
@@ -461,12 +463,12 @@ double optimize_two_phase_subspace(OptContext& c, SubspaceOps& ops, int k, int i
         DOT_CUDA_TRY(cudaMemcpyAsync(dQ.get(), Q0.data(), Q0.size() * 8, cudaMemcpyHostToDevice, s));
         project(dQ.get());
         orth(dQ.get());
-        DBuf<double2> FQ;
-        applyK(FQ);
+        DBuf<double2> FQ, FQP;
+        applyK(FQ, FQP);
         for (int t = 1; t < iters; ++t) {
             DOT_CUDA_TRY(cudaMemcpyAsync(dQ.get(), dY.get(), (size_t)n * blk * 8, cudaMemcpyDeviceToDevice, s));
             orth(dQ.get());
-            applyK(FQ);
+            applyK(FQ, FQP);
         }
         // Rayleigh-Ritz: H = Q^T Y (device), top eigenvector e (host), q = Q e
         DBuf<double> dH(c.arena, (size_t)blk * blk);
@@ -503,27 +505,30 @@ double optimize_two_phase_subspace(OptContext& c, SubspaceOps& ops, int k, int i
         // fields of the new column from the last block's fields (no extra solve)
         std::vector<double> ge(blk);
         for (int j = 0; j < blk; ++j) ge[j] = scale * e[j];
-        newfield = combine(FQ, blk, ge, 1);
+        newfield = combine(FQ, blk, ge, 1, K);
+        newfieldP = combine(FQP, blk, ge, 1, nP);
     };
-    auto append_field = [&](DBuf<double2>& Fm, int cols, const DBuf<double2>& nfld) {
-        DBuf<double2> out(c.arena, (size_t)nf * (cols + 1) * K);
+    auto append_field = [&](DBuf<double2>& Fm, int cols, const DBuf<double2>& nfld, int L) {
+        DBuf<double2> out(c.arena, (size_t)nf * (cols + 1) * L);
         for (int f = 0; f < nf; ++f) {
-            DOT_CUDA_TRY(cudaMemcpyAsync(out.get() + (size_t)f * (cols + 1) * K, Fm.get() + (size_t)f * cols * K,
-                                         (size_t)cols * K * sizeof(double2), cudaMemcpyDeviceToDevice, s));
-            DOT_CUDA_TRY(cudaMemcpyAsync(out.get() + ((size_t)f * (cols + 1) + cols) * K, nfld.get() + (size_t)f * K,
-                                         (size_t)K * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+            DOT_CUDA_TRY(cudaMemcpyAsync(out.get() + (size_t)f * (cols + 1) * L, Fm.get() + (size_t)f * cols * L,
+                                         (size_t)cols * L * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+            DOT_CUDA_TRY(cudaMemcpyAsync(out.get() + ((size_t)f * (cols + 1) + cols) * L, nfld.get() + (size_t)f * L,
+                                         (size_t)L * sizeof(double2), cudaMemcpyDeviceToDevice, s));
         }
         sync();
         Fm = std::move(out);
     };
     // ---- phase two: add a source (Theorem 3.7), then a detector (Theorem 3.6)
     for (int step = 0; step < k; ++step) {
-        DBuf<double2> nfz, nfy;
-        add_step(0, W, a, YV, b, X0s, step, nfz);
-        append_field(ZW, a, nfz);
+        DBuf<double2> nfz, nfy, nfzP, nfyP;
+        add_step(0, W, a, YV, b, X0s, step, nfz, nfzP);
+        append_field(ZW, a, nfz, K);
+        append_field(ZWP, a, nfzP, nP);
         ++a;
-        add_step(1, V, b, ZW, a, X0d, step, nfy);
-        append_field(YV, b, nfy);
+        add_step(1, V, b, ZW, a, X0d, step, nfy, nfyP);
+        append_field(YV, b, nfy, K);
+        append_field(YVP, b, nfyP, nP);
         ++b;
     }
     DBuf<double2> J = contract(YV.get(), b, ZW.get(), a);
@@ -533,6 +538,7 @@ double optimize_two_phase_subspace(OptContext& c, SubspaceOps& ops, int k, int i
     double obj = 0;
     DOT_CUDA_TRY(cudaMemcpyAsync(&obj, d_obj.get(), 8, cudaMemcpyDeviceToHost, s));
     sync();
+    ops.finish(W, a, ZWP, V, b, YVP);      // the optimized W, V and their fields on P -> field caches
     return obj;
 }
 

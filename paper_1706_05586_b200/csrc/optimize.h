@@ -28,12 +28,24 @@ double optimize_two_phase(OptContext& c, int k, std::vector<double>& W, int ls, 
 // C-ABI layer (they run the batched multi-shift CG kernels; no host synchronisation needed):
 struct SubspaceOps {
     // fields of point combinations on the support S: side 0 = B coeff (sources), 1 = C coeff
-    // (detectors); coeff device [n_side][ncols] row-major; out device [nf][ncols][K]
-    std::function<void(int side, const double* d_coeff, int ncols, double2* out)> fields;
+    // (detectors); coeff device [n_side][ncols] row-major; out device [nf][ncols][K], outP the
+    // same fields on the samples P [nf][ncols][nP]
+    std::function<void(int side, const double* d_coeff, int ncols, double2* out, double2* outP)> fields;
     // solve A_f x = w_f for nvec right-hand sides supported on S (w device [nf][nvec][K]) and
     // return b_s^T x (side 0, sources; b_s = theta e_s / cell volume) or c_d^T x (side 1):
     // out device [nf][nvec][n_side]
     std::function<void(const double2* w, int nvec, int side, double2* out)> solve_support;
+    // fields of the starting W (ns x ls) and V (nd x ld) on S, zw [nf][ls][K], yv [nf][ld][K],
+    // and on P, zwP [nf][ls][nP], yvP [nf][ld][nP]: from the library's field caches when the
+    // preceding jacobian / misfit call solved them, else both sides in one joint batch
+    std::function<void(const std::vector<double>& W, int ls, const std::vector<double>& V, int ld, double2* zw,
+                       double2* yv, double2* zwP, double2* yvP)>
+        start_fields;
+    // hands the optimized W (ns x a), V (nd x b) and their fields on P (ownership moves) to the
+    // library's field caches: a following jacobian / misfit with these W, V needs no solves
+    std::function<void(const std::vector<double>& W, int a, DBuf<double2>& zwP, const std::vector<double>& V, int b,
+                       DBuf<double2>& yvP)>
+        finish;
 };
 
 // Two-phase replacement where the add steps (Theorems 3.7, 3.6) use `iters` steps of

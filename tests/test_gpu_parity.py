@@ -276,6 +276,17 @@ def test_optimize_directions_subspace_parity(dot, iters, block):
         # solve accounting: W and V fields once, then 2 solves per block vector per step per frequency
         nf = len(cfg.freqs_hz)
         assert st["rhs_solved"] == nf * (4 + 3) + 2 * k * iters * 2 * block * nf
+        # the optimized W, V leave their fields (kept by combination, added from the last
+        # block's solves) in the caches: J(W_hat, V_hat) needs no solves and matches the oracle
+        g.reset_stats()
+        J2 = g.jacobian(Wg, Vg)
+        assert g.stats()["rhs_solved"] == 0
+        assert rel(J2, jacobian(prob, wl.p, Wg, Vg)) < 1e-7
+    # starting fields from the caches: after J(W, V) the subspace step solves only its blocks
+    g.jacobian(W, V)
+    g.reset_stats()
+    g.optimize_directions_subspace(1, W, V, X0s_all[:, :block], X0d_all[:, :block], iters=iters)
+    assert g.stats()["rhs_solved"] == 2 * iters * 2 * block * len(cfg.freqs_hz)
 
 
 def test_optimize_directions_subspace_converges_to_exact(dot):
