@@ -252,8 +252,10 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
     const int ntiles = a.tl.ntiles;
     const int tile = blockIdx.x % ntiles, zc = a.zc0 + blockIdx.x / ntiles;
     const int yrow = a.pair0 + (int)blockIdx.y;                    // split launches: rows [pair0, pair0 + ny)
-    const int pair = a.act ? a.act[yrow] : yrow;                   // active-list compaction (tail passes)
-    if (pair < 0) return;                                          // slot past the active count
+    // programmatic dependent launch: the next pass of the stream may be scheduled now; its CTAs
+    // set up their shared memory on free SMs and block at griddepcontrol.wait below until this
+    // grid has completed and flushed (no-ops when launched without the attribute)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // x split (wide rows): tile = (row tile ty, x part xp); the slot rows are nx = the part's
     // xw columns plus 2 halo columns on each side (local column c = global column cx0 + c)
     constexpr bool XS1 = XS_ == 1;                     // compile-time: no x split
@@ -288,7 +290,6 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
     int2* s_samp = reinterpret_cast<int2*>(scratch + 32 * kNumPartials);   // [nz] sample ranges
     __shared__ PairScalars sh_sc;
 
-    if (threadIdx.x < 32) pass_scalars(a, pair, blockIdx.x == 0, &sh_sc);
     {   // rows outside the domain (edge tiles only) must read as zero (Dirichlet y faces):
         // the p rows of every ring slot outside [rlo, rhi) and the Rbuf rows outside
         // [rlo - 1, rhi - 1); nothing else is read before it is written
@@ -321,6 +322,12 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bars[q])), "r"((int)blockDim.x));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    // everything above touches shared memory and set_params-time tables only; everything below
+    // reads what the previous kernels of the stream wrote (active list, partial sums, r, p)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int pair = a.act ? a.act[yrow] : yrow;                   // active-list compaction (tail passes)
+    if (pair < 0) return;                                          // slot past the active count
+    if (threadIdx.x < 32) pass_scalars(a, pair, blockIdx.x == 0, &sh_sc);
     __syncthreads();
     if (!sh_sc.active) return;
     const int kin = a.k & 1, kout = kin ^ 1;      // pass 0 reads p_{-1} = 0 (zeroed buffer), beta_0 = 0
@@ -1000,7 +1007,20 @@ static void launch_pass_ns(const PassArgs& a, int nb, cudaStream_t s) {
     }
     ensure_smem(k, a.tl.smem);
     dim3 grid(a.tl.ntiles * a.nzch, nb);
-    k<<<grid, a.tl.threads, a.tl.smem, s>>>(a);
+    // programmatic dependent launch: a pass that follows a pass
+    // in the stream is scheduled while its predecessor drains; DOT_CG_PDL=0 launches plainly
+    static const bool pdl = !(std::getenv("DOT_CG_PDL") && std::atoi(std::getenv("DOT_CG_PDL")) == 0);
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = dim3(a.tl.threads);
+    lc.dynamicSmemBytes = a.tl.smem;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl ? 1 : 0;
+    DOT_CUDA_TRY(cudaLaunchKernelEx(&lc, k, a));
     DOT_CUDA_TRY(cudaGetLastError());
 }
 
