@@ -1160,6 +1160,8 @@ int dot_create(const dot_config* cfg, dot_problem** out) {
             const char* eXS = std::getenv("DOT_CG_XS");
             P->tl = cg_tiling(P->nx, P->ny, P->nz, ePD ? std::max(1, std::atoi(ePD)) : 2, eTY ? std::atoi(eTY) : 0,
                               eRW ? std::atoi(eRW) : 0, eNM && std::atoi(eNM) != 0, eXS ? std::atoi(eXS) : 0);
+            const char* ePL = std::getenv("DOT_CG_PDL");
+            P->tl.pdl = !(ePL && std::atoi(ePL) == 0);
         }
         P->pc = PalsConst{P->nx, P->ny, P->nz, P->n_rbf, P->hx, P->hy, P->hz, P->gamma, P->eps, P->cutoff,
                           P->mua_in, P->mua_out};

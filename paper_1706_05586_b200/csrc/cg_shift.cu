@@ -1008,8 +1008,7 @@ static void launch_pass_ns(const PassArgs& a, int nb, cudaStream_t s) {
     ensure_smem(k, a.tl.smem);
     dim3 grid(a.tl.ntiles * a.nzch, nb);
     // programmatic dependent launch: a pass that follows a pass
-    // in the stream is scheduled while its predecessor drains; DOT_CG_PDL=0 launches plainly
-    static const bool pdl = !(std::getenv("DOT_CG_PDL") && std::atoi(std::getenv("DOT_CG_PDL")) == 0);
+    // in the stream is scheduled while its predecessor drains (tl.pdl; DOT_CG_PDL=0 at dot_create launches plainly)
     cudaLaunchConfig_t lc = {};
     lc.gridDim = grid;
     lc.blockDim = dim3(a.tl.threads);
@@ -1019,7 +1018,7 @@ static void launch_pass_ns(const PassArgs& a, int nb, cudaStream_t s) {
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = at;
-    lc.numAttrs = pdl ? 1 : 0;
+    lc.numAttrs = a.tl.pdl ? 1 : 0;
     DOT_CUDA_TRY(cudaLaunchKernelEx(&lc, k, a));
     DOT_CUDA_TRY(cudaGetLastError());
 }

@@ -21,6 +21,7 @@ struct CgTiling {
     int nxl = 0;          // slot row width: nx (xs = 1) or ceil(nx / xs) + 4 (2 halo columns per side)
     int nty = 0;          // row tiles (sample offsets are per (plane, row tile))
     size_t smem = 0;
+    bool pdl = true;      // passes launched with programmatic stream serialization (DOT_CG_PDL=0: plain)
 };
 // prefetch: planes loaded ahead (1..3; slots = prefetch + 2); want_ty > 0 forces the tile height,
 // want_rows > 0 the rows per thread

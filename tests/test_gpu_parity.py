@@ -539,3 +539,28 @@ def test_mid_size_sketched_panels_take_the_gathered_kernel(dot):
     assert st["contract_flops"] < st["contract_flops_dense"]      # block-sparse
     assert st["contract_dmma_flops"] == 0                          # not the segment GEMM
     assert rel(J, jacobian(prob, wl.p, W, V)) < 1e-7
+
+
+def test_dependent_launch_is_bitwise_neutral(dot, monkeypatch):
+    """The passes are launched with programmatic stream serialization (DESIGN.md "Pass launch
+    overlap"); DOT_CG_PDL=0 at problem creation launches them plainly.  The launch mode only
+    moves the shared-memory set-up ahead of the previous pass's completion, so sampled solutions,
+    iteration counts and the Jacobian must be bit-identical — a pass that read r, p or the active
+    list before the previous pass had finished would differ.  Small batches (one wave, z chunks:
+    the case in which the next pass is resident early) and a multi-wave batch; the default mode
+    is also checked against the oracle."""
+    for n, src, det in (((32, 32, 12), (3, 2), (2, 3)), ((64, 37, 9), (6, 5), (5, 5))):
+        cfg = small_config(n=n, L=(4.0, 4.0, 2.0), src=src, det=det, eps=0.5, seed=5)
+        prob, wl = small_problem(cfg)
+        out = []
+        for mode in ("1", "0"):
+            monkeypatch.setenv("DOT_CG_PDL", mode)
+            g = gpu_problem(dot, cfg, prob, wl)
+            X = g.solve_sampled(0)
+            J = g.jacobian(None, None)
+            out.append((X.copy(), J.copy(), g.stats()["rhs_iterations"]))
+            del g
+        assert out[0][2] == out[1][2]
+        assert np.array_equal(out[0][0], out[1][0])
+        assert np.array_equal(out[0][1], out[1][1])
+        assert rel(out[0][1], jacobian(prob, wl.p, np.eye(cfg.n_s), np.eye(cfg.n_d))) < 1e-7

@@ -16,7 +16,7 @@ PCMD="python bench.py --profile --no-cpu-baseline --no-e2e"
 timeout 600 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 600 $PCMD > gpurun_out/plain2.log 2>&1 && \
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:cg_pass_kernel -s 420 -c 1 -o gpurun_out/prof_pass $PCMD > gpurun_out/ncu_pass.log 2>&1; echo "ncu pass rc=$?"
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:cg_pass_kernel -s 900 -c 1 -o gpurun_out/prof_pass $PCMD > gpurun_out/ncu_pass.log 2>&1; echo "ncu pass rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:seg_tma_gemm -c 1 -o gpurun_out/prof_contract $PCMD > gpurun_out/ncu_contract.log 2>&1; echo "ncu contract rc=$?"
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:cg_pass_kernel -s 40 -c 1 -o gpurun_out/prof_pass128 python tools/pass_bench.py all128 512 1 > gpurun_out/ncu_pass128.log 2>&1; echo "ncu pass128 rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:cg_pass_kernel -s 100 -c 1 -o gpurun_out/prof_pass96 python tools/pass_bench.py opt96 20 1 > gpurun_out/ncu_pass96.log 2>&1; echo "ncu pass96 rc=$?"
