@@ -290,18 +290,22 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
     int2* s_samp = reinterpret_cast<int2*>(scratch + 32 * kNumPartials);   // [nz] sample ranges
     __shared__ PairScalars sh_sc;
 
-    {   // rows outside the domain (edge tiles only) must read as zero (Dirichlet y faces):
+    auto prologue_fill = [&]() {
+        // rows outside the domain (edge tiles only) must read as zero (Dirichlet y faces):
         // the p rows of every ring slot outside [rlo, rhi) and the Rbuf rows outside
         // [rlo - 1, rhi - 1); nothing else is read before it is written
         const int rlo_ = max(0, 2 - j0), rhi_ = min(TY + 4, ny - j0 + 2);
         const int nlo = rlo_ * nx, nhi = (TY + 4 - rhi_) * nx;
         if (nlo + nhi > 0) {
             const int per = nlo + nhi;
-            for (int i = threadIdx.x; i < NS * per; i += blockDim.x) {
-                const int q = i / per, e = i - q * per;
-                const int el = e < nlo ? e : rhi_ * nx + (e - nlo);
-                slots[(size_t)q * slotW + slotE + el] = cmk(0, 0);
-            }
+            // (x split: every tensor copy zero-fills its box outside the domain; the prologue writes
+            // nothing into the ring slots, so the first copies may be issued before the barrier)
+            if (xs == 1)
+                for (int i = threadIdx.x; i < NS * per; i += blockDim.x) {
+                    const int q = i / per, e = i - q * per;
+                    const int el = e < nlo ? e : rhi_ * nx + (e - nlo);
+                    slots[(size_t)q * slotW + slotE + el] = cmk(0, 0);
+                }
             const int blo = max(0, rlo_ - 1) * nx, bhi_r = max(0, rhi_ - 1);
             const int bper = blo + (TY + 2 - min(TY + 2, bhi_r)) * nx;
             for (int i = threadIdx.x; i < 3 * bper; i += blockDim.x) {
@@ -314,7 +318,8 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
             for (int g = threadIdx.x; g < nz; g += blockDim.x)
                 s_samp[g] = XS1 ? make_int2(a.samp_off[g * ntiles + tile], a.samp_off[g * ntiles + tile + 1])
                                 : make_int2(a.samp_off[g * a.tl.nty + ty], a.samp_off[g * a.tl.nty + ty + 1]);
-    }
+    };
+    prologue_fill();
     if (threadIdx.x == 0) {
         for (int q = 0; q < NS; ++q)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bars[q])), "r"(1));
@@ -327,9 +332,6 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int pair = a.act ? a.act[yrow] : yrow;                   // active-list compaction (tail passes)
     if (pair < 0) return;                                          // slot past the active count
-    if (threadIdx.x < 32) pass_scalars(a, pair, blockIdx.x == 0, &sh_sc);
-    __syncthreads();
-    if (!sh_sc.active) return;
     const int kin = a.k & 1, kout = kin ^ 1;      // pass 0 reads p_{-1} = 0 (zeroed buffer), beta_0 = 0
     const double2* __restrict__ Rin = a.R[kin] + (size_t)pair * N;
     const double2* __restrict__ Pin = a.Pv[kin] + (size_t)pair * N;
@@ -393,8 +395,27 @@ __global__ void __launch_bounds__(MAXT, 1) cg_pass_kernel(const __grid_constant_
                 "l"(a.mu + g), "r"(mu_bytes), "r"(bar)
                 : "memory");
     };
+    // First planes: the copies land in slot rows no thread writes in the prologue (unsplit rows: the
+    // in-domain rows; x split: whole boxes, which the prologue leaves alone), so thread 0 issues them
+    // before the scalars and the copy latency overlaps pass_scalars and the barrier.
+    int npre = 0;
     if (threadIdx.x == 0)
-        for (int z = a1; z < a1 + PD && z < b1; ++z) issue(z, z - a1);
+        for (int z = a1; z < a1 + PD && z < b1; ++z, ++npre) issue(z, z - a1);
+    if (threadIdx.x < 32) pass_scalars(a, pair, blockIdx.x == 0, &sh_sc);
+    __syncthreads();
+    if (!sh_sc.active) {
+        // a finished pair still in the launch: the copies in flight must land before the CTA exits
+        if (threadIdx.x == 0)
+            for (int q = 0; q < npre; ++q)
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\t"
+                    "WAITX_%=:\n\t"
+                    "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                    "@!p bra WAITX_%=;\n\t}" ::"r"(bar0 + 8 * q),
+                    "r"(0)
+                    : "memory");
+        return;
+    }
 
     // ---- per-thread geometry: rows r0 .. r0 + RPT - 1 of column x
     const int t = threadIdx.x;
