@@ -39,7 +39,9 @@ UNIT = "RHS solves/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: 10 for full64 -- ~3 s, so that one host or NVML hiccup does not "
+                         "move the line --, 30 for sketch32, 3 for opt96, 1 for all128)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="full64")
@@ -47,7 +49,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="one untimed step (for ncu launch lists)")
     ap.add_argument("--oracle-sample", default=None, help=argparse.SUPPRESS)
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 3 if args.impl == "reference" else \
+            {"full64": 10, "sketch32": 30, "opt96": 3, "all128": 1}.get(args.config, 3)
+    return args
 
 
 # ------------------------------------------------------------------ helpers
