@@ -76,8 +76,14 @@ struct dot_problem {
     // wave tail is filled by the other half's CTAs) and its fork / join events
     cudaStream_t side = nullptr;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    // stream of the folds (they run beside the next passes; history ring of two fold periods)
+    cudaStream_t fold_stream = nullptr;
+    cudaEvent_t fold_in = nullptr, fold_done = nullptr;
 
     ~dot_problem() {
+        if (fold_in) cudaEventDestroy(fold_in);
+        if (fold_done) cudaEventDestroy(fold_done);
+        if (fold_stream) cudaStreamDestroy(fold_stream);
         if (fork_ev) cudaEventDestroy(fork_ev);
         if (join_ev) cudaEventDestroy(join_ev);
         if (side) cudaStreamDestroy(side);
@@ -228,7 +234,16 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, c
     const size_t N = P->N;
     const int nf = P->n_freq, nP = nP_out;
     const int npairs = sp.nseeds / 2;
-    const int hist = dense ? 8 : kHist;      // dense solutions sample every node: fold every poll group
+    // Sampled solves of less than two waves of CTAs (latency-bound passes: the sketched regimes) fold
+    // every kHist passes on a side stream while the next passes run; their history rings hold two fold
+    // periods (the passes of one period write one half while the fold reads the other).  Larger
+    // batches fold in the pass stream (beside multi-wave passes the fold only competes for HBM:
+    // measured equal step time).  Dense solutions sample every node: they fold every poll
+    // group in the pass stream.  DOT_CG_FOLD_SIDE=0 / 1 forces either (sampled solves).
+    const char* eFS = std::getenv("DOT_CG_FOLD_SIDE");
+    const bool fold_side = !dense && (eFS ? std::atoi(eFS) != 0 : (long long)P->tl.ntiles * npairs < 2LL * P->num_sms);
+    const int fold_n = dense ? 8 : kHist;    // passes per fold
+    const int hist = fold_side ? 2 * fold_n : fold_n;
     const int nsl = dense ? 1 : nf;
     const size_t ppb = per_pair_bytes(P, nP, hist, nsl);
     size_t fit = P->arena.largest_free() / ppb;
@@ -368,7 +383,7 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, c
         // so the GPU never idles on the host round trip (a group launched after the last
         // pair finished runs as no-ops).  Every kHist passes the fold kernel applies the
         // shifted recurrences of those passes on the samples.
-        int k = 0, g = 0, kf = 0;
+        int k = 0, g = 0, kf = 0, nfold = 0;
         size_t ev = 0;
         for (;;) {
             if (P->timing) DOT_CUDA_TRY(cudaEventRecord(event_at(P, ev++), P->stream));
@@ -407,10 +422,25 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, c
                 DOT_CUDA_TRY(cudaStreamWaitEvent(P->stream, P->join_ev, 0));
             }
             if (P->timing) DOT_CUDA_TRY(cudaEventRecord(event_at(P, ev++), P->stream));
-            if (k - kf >= hist) {
+            if (k - kf >= fold_n) {
                 fa.k0 = kf;
                 fa.k1 = k;
-                launch_cg_fold(fa, P->stream);
+                if (fold_side) {
+                    if (!P->fold_stream) {
+                        DOT_CUDA_TRY(cudaStreamCreateWithFlags(&P->fold_stream, cudaStreamNonBlocking));
+                        DOT_CUDA_TRY(cudaEventCreateWithFlags(&P->fold_in, cudaEventDisableTiming));
+                        DOT_CUDA_TRY(cudaEventCreateWithFlags(&P->fold_done, cudaEventDisableTiming));
+                    }
+                    // the passes from here on overwrite the ring half the previous fold read
+                    if (nfold > 0) DOT_CUDA_TRY(cudaStreamWaitEvent(P->stream, P->fold_done, 0));
+                    DOT_CUDA_TRY(cudaEventRecord(P->fold_in, P->stream));          // passes [kf, k) done
+                    DOT_CUDA_TRY(cudaStreamWaitEvent(P->fold_stream, P->fold_in, 0));
+                    launch_cg_fold(fa, P->fold_stream);
+                    DOT_CUDA_TRY(cudaEventRecord(P->fold_done, P->fold_stream));
+                    ++nfold;
+                } else {
+                    launch_cg_fold(fa, P->stream);
+                }
                 P->stats.kernel_launches++;
                 kf = k;
             }
@@ -430,6 +460,7 @@ std::vector<int32_t> solve_batch(dot_problem* P, const std::vector<Seg>& segs, c
         }
         fa.k0 = kf;
         fa.k1 = k;
+        if (nfold > 0) DOT_CUDA_TRY(cudaStreamWaitEvent(P->stream, P->fold_done, 0));   // folds are ordered
         launch_cg_fold(fa, P->stream);
         launch_cg_finalize(fa, P->op, XP, nP, domap.get(), samp_nodes, P->stream);
         P->stats.kernel_launches += 2;
@@ -1212,7 +1243,11 @@ size_t dot_workspace_bytes(const dot_problem* P, int32_t max_rhs) {
     const size_t pairs = ((size_t)std::max(max_rhs, 1) + 2 * P->n_freq - 1) / (2 * P->n_freq) + 1;
     // dense solutions (dot_solve: every node sampled) of up to 3 complex right-hand sides
     const size_t dense = 3 * per_pair_bytes(P, (int)N, 8, 1) + 6 * N * sizeof(double2);
-    return fixed + std::max(pairs * per_pair_bytes(P, (int)Kb, kHist, P->n_freq), dense) + 64 * Arena::kAlign;
+    // (batches of less than two waves keep a history ring of two fold periods)
+    const size_t small_pairs = std::min(pairs, (size_t)(2 * P->num_sms / std::max(P->tl.ntiles, 1) + 1));
+    const size_t ring2 = small_pairs * (per_pair_bytes(P, (int)Kb, 2 * kHist, P->n_freq) -
+                                        per_pair_bytes(P, (int)Kb, kHist, P->n_freq));
+    return fixed + std::max(pairs * per_pair_bytes(P, (int)Kb, kHist, P->n_freq) + ring2, dense) + 64 * Arena::kAlign;
 }
 
 int dot_bind_workspace(dot_problem* P, void* ptr, size_t bytes) {

@@ -1116,7 +1116,7 @@ void launch_cg_init(const PassArgs& a, int nb, cudaStream_t s, int zc_own) {
 
 void launch_cg_fold(const FoldArgs& f, cudaStream_t s) {
     if (f.k1 <= f.k0 || f.s1 <= f.s0 || f.npairs <= 0) return;
-    if (f.k1 - f.k0 > kHist || f.hist > kHist) throw Error(DOT_ERR_ARG, "fold span exceeds the history ring");
+    if (f.k1 - f.k0 > kHist || f.hist > 2 * kHist) throw Error(DOT_ERR_ARG, "fold span exceeds the history ring");
     dim3 grid((f.s1 - f.s0 + 127) / 128, f.npairs);
     switch (f.nsl) {
         case 1: cg_fold_kernel<1><<<grid, 128, 0, s>>>(f); break;

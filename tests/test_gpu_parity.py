@@ -548,19 +548,22 @@ def test_dependent_launch_is_bitwise_neutral(dot, monkeypatch):
     iteration counts and the Jacobian must be bit-identical — a pass that read r, p or the active
     list before the previous pass had finished would differ.  Small batches (one wave, z chunks:
     the case in which the next pass is resident early) and a multi-wave batch; the default mode
-    is also checked against the oracle."""
+    is also checked against the oracle.  The same holds for the fold of the shifted recurrences
+    running on its side stream (two-period history ring) or in the pass stream."""
     for n, src, det in (((32, 32, 12), (3, 2), (2, 3)), ((64, 37, 9), (6, 5), (5, 5))):
         cfg = small_config(n=n, L=(4.0, 4.0, 2.0), src=src, det=det, eps=0.5, seed=5)
         prob, wl = small_problem(cfg)
         out = []
-        for mode in ("1", "0"):
+        for mode, fold in (("1", "1"), ("0", "0"), ("1", "0")):
             monkeypatch.setenv("DOT_CG_PDL", mode)
+            monkeypatch.setenv("DOT_CG_FOLD_SIDE", fold)   # folds beside the next passes / in the pass stream
             g = gpu_problem(dot, cfg, prob, wl)
             X = g.solve_sampled(0)
             J = g.jacobian(None, None)
             out.append((X.copy(), J.copy(), g.stats()["rhs_iterations"]))
             del g
-        assert out[0][2] == out[1][2]
-        assert np.array_equal(out[0][0], out[1][0])
-        assert np.array_equal(out[0][1], out[1][1])
+        for o in out[1:]:
+            assert out[0][2] == o[2]
+            assert np.array_equal(out[0][0], o[0])
+            assert np.array_equal(out[0][1], o[1])
         assert rel(out[0][1], jacobian(prob, wl.p, np.eye(cfg.n_s), np.eye(cfg.n_d))) < 1e-7
